@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""MCSF throughput benchmark (BASELINE.json metric: pixel*samples/s at fixed M).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config I] [--impl ours|reference]
+                    [--mode bands|samples]
+
+One "step" = one bf_vec_filter call: the whole hot path (fused MC kernel +
+normalisation) over one synthetic image of BASELINE config I (default 5,
+the 8192x8192 scaling config; see DESIGN.md §7 for why). Inputs are resident
+in HBM when the timed region starts; `e2e` times bf_vec_filter_host (pinned
+host buffers, H2D + filter + D2H inside the timed region).
+
+N > 1 (torchrun, one rank per GPU, NCCL): `--mode bands` (default) splits the
+image into row bands with an r-row halo (no communication, strong scaling);
+`--mode samples` splits the M samples and sums the (d+1) accumulator planes
+with one NCCL reduce-scatter (strong scaling).
+
+`--impl reference` times the CPU oracle (Algorithm 1 in fp64, OpenMP) on a
+bounded row band of the same workload on this host's cores.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "pixel*samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="bands", choices=["bands", "samples"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks under load (NVML), sampled in a background thread during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {  # nvmlClocksEventReason bits
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def fp32_peak_tflops(mhz):
+    """FP32 pipe peak: 148 SMs x 128 FFMA lanes/clk x 2 flop/FFMA x clock."""
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def algorithmic_flops_per_px_sample(d, r):
+    """Algorithmic FP32 work per pixel-sample: phase d FMA, modulation
+    2d MUL, two (2r+1)-tap passes over 2(d+1) channels, accumulate 2(d+1) FMA.
+    FMA = 2 flops, MUL = 1 flop."""
+    fma = d + 2 * 2 * (d + 1) * (2 * r + 1) + 2 * (d + 1)
+    return 2 * fma + 2 * d
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_sample(cfg, rows=8, samples=None):
+    """Time Algorithm 1 (oracle/native, fp64 OpenMP) on output rows [y0, y0+rows) in
+    the middle of the image with the first `samples` draws. Returns (px*samples/s, info)."""
+    from oracle import draws, native
+    from oracle import plan as oplan
+    from workloads import make_image_rows
+    M = cfg.M if samples is None else min(samples, cfg.M)
+    y0 = max(0, min(cfg.H - rows, cfg.H // 2 - rows // 2))
+    rows = min(rows, cfg.H)
+    s0, s1 = native.slab_bounds(cfg.H, y0, rows, cfg.radius)
+    slab = make_image_rows(cfg, s0, s1)
+    Q, a = oplan.diagonalize(cfg.C_array)
+    Y = draws.y_draws(cfg.seed, cfg.M, cfg.d, cfg.N)[:M]
+    t0 = time.perf_counter()
+    native.mcsf_alg1(slab, cfg.H, s0, y0, rows, Q, a, cfg.N, Y, cfg.sigma_s)
+    dt = time.perf_counter() - t0
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    info = {"rows": [y0, y0 + rows], "samples": M, "seconds": dt, "threads": threads}
+    return rows * cfg.W * M / dt, info
+
+
+def cpu_sample_size(cfg):
+    # ~10-30 s of fp64 work on an 8-core host for the default sample
+    rows = 8 if cfg.H >= 8 else cfg.H
+    lane_ops = cfg.W * (2 * rows + 2 * cfg.radius) * 2 * (cfg.d + 1) * (2 * cfg.radius + 1)
+    samples = max(1, min(cfg.M, int(2.0e11 / lane_ops)))
+    return rows, samples
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rows, samples = cpu_sample_size(cfg)
+    samples = max(1, samples // 4)          # each step a bounded sample (whole run: minutes)
+    for _ in range(args.warmup):
+        oracle_sample(cfg, rows, samples)
+    vals, secs = [], 0.0
+    for _ in range(args.steps):
+        v, info = oracle_sample(cfg, rows, samples)
+        vals.append(v)
+        secs += info["seconds"]
+    value = args.steps * rows * cfg.W * samples / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pixel*samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "d": cfg.d, "sigma_s": cfg.sigma_s,
+                   "N": cfg.N, "M": cfg.M, "seed": cfg.seed},
+        "cpu_baseline": {"value": value, "unit": "pixel*samples/s", "cores": info["threads"],
+                         "kind": "oracle",
+                         "sample": f"output rows {info['rows']} x {cfg.W} cols, first {samples} of "
+                                   f"{cfg.M} samples, per step"},
+        "e2e": {"value": value, "unit": "pixel*samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1605_02164_b200 import Plan
+    from workloads import make_image_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    r = cfg.radius
+    plan = Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, cfg.M, cfg.seed,
+                value_range=cfg.value_range)
+    plan.sample_freqs()
+
+    # this rank's work
+    if world == 1 or args.mode == "samples":
+        y0, y1, s0, s1 = 0, cfg.H, 0, cfg.H
+    else:
+        y0 = cfg.H * rank // world
+        y1 = cfg.H * (rank + 1) // world
+        s0, s1 = max(0, y0 - r), min(cfg.H, y1 + r)
+    f_host = torch.from_numpy(make_image_rows(cfg, s0, s1))
+    f = f_host.to(dev)
+    rows = y1 - y0
+    out = torch.empty((cfg.d, rows, cfg.W), dtype=torch.float32, device=dev)
+    k0 = cfg.M * rank // world if args.mode == "samples" else 0
+    k1 = cfg.M * (rank + 1) // world if args.mode == "samples" else cfg.M
+    PZ = None
+    if args.mode == "samples" and world > 1:
+        rpb = (cfg.H + world - 1) // world
+        PZ = torch.empty((cfg.d + 1) * cfg.H * cfg.W, dtype=torch.float32, device=dev)
+        band0 = rank * rpb
+        band1 = min(cfg.H, band0 + rpb)
+        PZ_band = torch.empty((cfg.d + 1) * (band1 - band0) * cfg.W, dtype=torch.float32, device=dev)
+        counts = [(cfg.d + 1) * (min(cfg.H, (g + 1) * rpb) - g * rpb) * cfg.W for g in range(world)]
+        out = torch.empty((cfg.d, band1 - band0, cfg.W), dtype=torch.float32, device=dev)
+
+    stream = torch.cuda.current_stream()
+    launches_per_step = 0
+
+    def step():
+        nonlocal launches_per_step
+        if world == 1:
+            plan.filter(f, out)
+            launches_per_step = 3
+        elif args.mode == "bands":
+            plan.filter_rows(f, s0, y0, y1, out)
+            launches_per_step = 3
+        else:
+            plan.filter_partial(f, k0, k1, PZ, rows_per_band=rpb)
+            chunks = list(torch.split(PZ, counts))
+            dist.reduce_scatter(PZ_band, chunks)
+            plan.normalize(PZ_band, band0, band1, out)
+            launches_per_step = 4
+
+    flush = None
+    in_bytes = f.numel() * 4
+    l2_note = "inputs larger than L2 (126 MB)" if in_bytes > 256e6 else "L2 flushed between steps"
+    if in_bytes <= 256e6:
+        flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    plan.set_option("profile", 1)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(float(i))
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    fused_ns = plan.info("fused_ns_total")
+    fused_calls = plan.info("fused_calls")
+    plan.set_option("profile", 0)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_units = cfg.H * cfg.W * cfg.M * args.steps
+    value = total_units / (ms_max / 1e3)
+
+    # e2e through the C ABI with pinned host buffers (N = 1; bands: per-rank slabs)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        fh = f_host.pin_memory()
+        oh = torch.empty((cfg.d, cfg.H, cfg.W), dtype=torch.float32).pin_memory()
+        plan.filter_host(fh, oh)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        n_e2e = max(1, min(args.steps, 3))
+        for _ in range(n_e2e):
+            plan.filter_host(fh, oh)
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": cfg.H * cfg.W * cfg.M * n_e2e / e2e_s, "unit": "pixel*samples/s",
+               "h2d_bytes_per_step": fh.numel() * 4, "d2h_bytes_per_step": oh.numel() * 4,
+               "steps": n_e2e}
+
+    clocks = clk.summary()
+    pk = peaks()
+    mhz_max = clocks.get("sm_max_mhz") or pk.get("sm_max_mhz") or 1965.0
+    peak = fp32_peak_tflops(mhz_max)
+    fused_ms = fused_ns / 1e6 / max(1, fused_calls)
+    units_per_launch = rows * cfg.W * (k1 - k0)
+    flops = algorithmic_flops_per_px_sample(cfg.d, r) * units_per_launch
+    achieved = flops / (fused_ms / 1e3) / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "mcsf_fused_kernel", "fused_ms_per_launch": fused_ms,
+            "peak_source": f"FP32 pipe: 148 SM x 128 lanes x 2 flop x {mhz_max} MHz (sm_max)",
+            "frac_at_run_clock": (achieved / fp32_peak_tflops(clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
+            "flops_per_px_sample": algorithmic_flops_per_px_sample(cfg.d, r),
+            "fused_share_of_step": (fused_ns / 1e6) / ms if ms > 0 else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows_s, samples_s = cpu_sample_size(cfg)
+        v, info = oracle_sample(cfg, rows_s, samples_s)
+        cpu = {"value": v, "unit": "pixel*samples/s", "cores": info["threads"], "kind": "oracle",
+               "sample": f"output rows {info['rows']} x {cfg.W} cols, first {samples_s} of {cfg.M} samples "
+                         f"({info['seconds']:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pixel*samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "d": cfg.d, "sigma_s": cfg.sigma_s,
+                       "radius": r, "N": cfg.N, "M": cfg.M, "seed": cfg.seed,
+                       "parallelism": (f"{args.mode}{world}" if world > 1 else "single"),
+                       "l2": l2_note, "tile_rows": plan.info("tile_rows"), "groups": plan.info("groups")},
+            "mpix_per_s": cfg.H * cfg.W * args.steps / (ms_max / 1e3) / 1e6,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from workloads import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,198 @@
+/*
+ * bfvec.h -- C ABI of libbfvec.so: the Monte Carlo Shiftable Filter (MCSF) of
+ * arXiv 1605.02164 ("Fast bilateral filtering of vector-valued images") on
+ * NVIDIA B200 (sm_100a).
+ *
+ * The filter (Algorithm 1): given a vector-valued image
+ * f : Omega -> R^d, a spatial Gaussian omega with window
+ * [-3 sigma_s, 3 sigma_s]^2 (Eq. (1)) and a range Gaussian
+ * phi(x) = exp(-x^T C^-1 x / 2), the range kernel is replaced by a product of
+ * raised cosines of order N (Eq. (9)) and sampled with M
+ * binomial frequency vectors (Eq. (13)-(14)). The output is
+ *     S(i) = P(i) / Z(i),
+ *     Z(i) = sum_k Re[ conj(H_k(i)) (omega * H_k)(i) ],
+ *     P(i) = sum_k Re[ conj(H_k(i)) (omega * (H_k f))(i) ],
+ *     H_k(i) = exp(iota t_k . f(i)),  t_k = Q (Y_k o alpha / sqrt(N)),
+ * with Y_k = N - 2 X_k, X_k ~ B(N, 1/2)^d (Eq. (15)-(19), PAPER.md:172-202;
+ * readings R4, R6, R7 of DESIGN.md).
+ *
+ * Conventions shared by every entry point:
+ *  - Images are DEVICE pointers to planar float32 (d, rows, W): channel-major,
+ *    row-major within a channel, no padding, 4-byte aligned. The caller owns
+ *    them. C is a HOST pointer to a d x d row-major double matrix.
+ *  - Boundary: half-sample symmetric reflection (reading R1).
+ *  - All filter calls are stream-ordered and asynchronous on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream). Launch
+ *    failures are reported as BF_E_CUDA by the call that launched.
+ *  - A plan owns its device scratch (frequency table, partial sums,
+ *    diagnostics). One plan must not be used from two streams concurrently.
+ *  - No exceptions cross the ABI; every function returns a bf_status_t
+ *    (< 0 error, 0 ok, > 0 warning). On error no output is written.
+ *  - There is no CPU fallback: if no sm_100 device is present the calls that
+ *    launch kernels return BF_E_CUDA.
+ */
+#ifndef BFVEC_H
+#define BFVEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bf_vec_plan_s *bf_vec_plan_t;   /* opaque, owned by the library */
+
+typedef enum {
+    BF_OK = 0,
+    BF_E_ARG = -1,            /* invalid argument (sizes, pointers, ranges)           */
+    BF_E_NOT_SYMMETRIC = -2,  /* C not symmetric within 1e-12 relative   */
+    BF_E_NOT_POSDEF = -3,     /* an eigenvalue of C <= 1e-12 * max eigenvalue          */
+    BF_E_UNSUPPORTED = -4,    /* configuration outside the compiled kernel set         */
+    BF_E_CUDA = -5,           /* CUDA runtime / launch error                           */
+    BF_E_STATE = -6,          /* call order violated (e.g. filter before sample_freqs) */
+    BF_W_ALIAS = 1,           /* raised cosine leaves its main lobe on the data range  */
+    BF_W_SMALL_Z = 2          /* some pixel has Z/M < z_floor (output still written)   */
+} bf_status_t;
+
+/*
+ * bf_vec_plan -- Algorithm 1 setup, L210-214.
+ *   H, W      image height and width, >= 1
+ *   d         vector dimension, 1 <= d <= 8
+ *   sigma_s   spatial std-dev (pixels) > 0; window radius r = ceil(3 sigma_s) <= 64
+ *   C         host, d x d row-major symmetric positive-definite covariance (Eq. (1))
+ *   N         raised-cosine order, even, 2 <= N <= 64 (Eq. (9))
+ *   M         number of Monte Carlo samples (the paper's T), M >= 1
+ *   seed      Philox4x64-10 key (reading R9)
+ *   out       receives the plan handle
+ * Diagonalises C in fp64 (cyclic Jacobi; canonical order and signs of
+ * reading R8), builds the normalised fp32 taps (reading R3), picks the
+ * kernel instance, and allocates device scratch on the current device.
+ * Errors: BF_E_ARG, BF_E_NOT_SYMMETRIC, BF_E_NOT_POSDEF, BF_E_UNSUPPORTED, BF_E_CUDA.
+ */
+bf_status_t bf_vec_plan(int H, int W, int d, double sigma_s, const double *C, int N, int M,
+                        uint64_t seed, bf_vec_plan_t *out);
+
+/* Frees the plan and its device scratch (synchronises the plan's last stream). */
+void bf_vec_plan_destroy(bf_vec_plan_t plan);
+
+/*
+ * bf_vec_sample_freqs -- Alg. 1 L221 hoisted (Prop. 2):
+ * one device kernel draws X_kc = popcount(philox_word(k*d+c) & (2^N-1)),
+ * Y = N - 2X, and the fp32 frequency table t_k = Q (Y_k o alpha / sqrt(N))
+ * (computed in fp64, rounded once) into plan scratch. Must be called once
+ * before any filter call. Asynchronous on `stream`.
+ */
+bf_status_t bf_vec_sample_freqs(bf_vec_plan_t plan, void *stream);
+
+/*
+ * bf_vec_get_draws -- synchronous host copies for checking against the oracle.
+ *   X      (M, d) int32 binomial draws, or NULL
+ *   t      (M, d) float32 frequency table, or NULL
+ *   Q      (d, d) double row-major eigenbasis (columns q_k), or NULL
+ *   alpha  (d) double, or NULL
+ * Errors: BF_E_STATE if bf_vec_sample_freqs was never called (X, t).
+ */
+bf_status_t bf_vec_get_draws(bf_vec_plan_t plan, int32_t *X, float *t, double *Q, double *alpha);
+
+/*
+ * bf_vec_filter -- the whole hot path for all M samples: S = P / Z
+ * (Alg. 1). f, out: device planar (d, H, W) float32; out may not
+ * alias f. Returns BF_OK or BF_W_ALIAS (data leaves the raised cosine's main
+ * lobe; output still written). BF_W_SMALL_Z is reported by bf_vec_diag.
+ */
+bf_status_t bf_vec_filter(bf_vec_plan_t plan, const float *f, float *out, void *stream);
+
+/*
+ * bf_vec_filter_host -- bf_vec_filter on HOST buffers: copies f (d,H,W) to the
+ * device, filters, copies out back, and synchronises `stream`. Pinned host
+ * memory gives full PCIe bandwidth; pageable memory works but is slower.
+ */
+bf_status_t bf_vec_filter_host(bf_vec_plan_t plan, const float *f_host, float *out_host,
+                               void *stream);
+
+/*
+ * bf_vec_filter_partial -- raw sums over samples k in [k0, k1) only
+ * (0 <= k0 <= k1 <= M), for sample sharding (one NCCL sum afterwards).
+ *   PZ         device float32, (d+1) planes per row band: for band b covering
+ *              rows [b*rows_per_band, min(H, (b+1)*rows_per_band)) the block
+ *              (d+1, band_rows, W) is stored contiguously, bands in order.
+ *              Planes 0..d-1 hold P_c, plane d holds Z (raw, uncentred, no 1/M).
+ *   rows_per_band  1..H (H gives the plain (d+1, H, W) layout)
+ */
+bf_status_t bf_vec_filter_partial(bf_vec_plan_t plan, const float *f, int k0, int k1, float *PZ,
+                                  int rows_per_band, void *stream);
+
+/*
+ * bf_vec_normalize -- Alg. 1: out_c = P_c / Z for rows [row0, row1).
+ *   PZ_band   device (d+1, row1-row0, W) block as written by filter_partial
+ *             (and summed over shards)
+ *   out_band  device (d, row1-row0, W)
+ * Updates the plan's diagnostics (z_min, small-Z count; see bf_vec_diag).
+ */
+bf_status_t bf_vec_normalize(bf_vec_plan_t plan, const float *PZ_band, int row0, int row1,
+                             float *out_band, void *stream);
+
+/*
+ * bf_vec_filter_rows -- band sharding without communication: output rows
+ * [row0, row1) of the full H x W image from an input slab holding image rows
+ * [slab_row0, slab_row0 + slab_rows). The slab must contain every reflected
+ * row within r of the band (else BF_E_ARG).
+ *   slab      device (d, slab_rows, W)
+ *   out_band  device (d, row1-row0, W)
+ */
+bf_status_t bf_vec_filter_rows(bf_vec_plan_t plan, const float *slab, int slab_row0,
+                               int slab_rows, int row0, int row1, float *out_band, void *stream);
+
+/*
+ * bf_vec_direct -- the exact bilateral filter Eq. (2)-(3) on the
+ * same window and boundary, O(r^2) per pixel; the accuracy reference for PSNR.
+ * f, out: device planar (d, H, W) float32.
+ */
+bf_status_t bf_vec_direct(bf_vec_plan_t plan, const float *f, float *out, void *stream);
+
+/*
+ * bf_vec_diag -- synchronises the plan's last stream and returns diagnostics of
+ * the most recent filter/normalize call: z_min = min over pixels of Z/M and
+ * n_small_z = #pixels with Z/M < z_floor (default 0.05). Returns BF_W_SMALL_Z
+ * when n_small_z > 0.
+ */
+bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
+
+/*
+ * bf_vec_set_option -- tuning / policy knobs (all optional):
+ *   "z_floor"     threshold of the small-Z diagnostic (default 0.05)
+ *   "value_range" nominal data range R used for the alias warning (default 255)
+ *   "tile_rows"   force the row-tile height of the fused kernel (0 = auto)
+ *   "groups"      force the number of sample groups (0 = auto)
+ *   "profile"     1: record CUDA events around every fused-kernel launch on the
+ *                 launching stream (read back with bf_vec_plan_info
+ *                 "fused_ns_total" / "fused_calls"); 0: off. Setting it resets the totals.
+ * Errors: BF_E_ARG on an unknown name or invalid value.
+ */
+bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value);
+
+/*
+ * bf_vec_plan_info -- integers describing the plan (for tooling and tests):
+ *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
+ *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
+ *   "regs", "occupancy", "alias", and (option "profile") "fused_ns_total",
+ *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
+ *   an unknown name.
+ */
+bf_status_t bf_vec_plan_info(bf_vec_plan_t plan, const char *name, long long *value);
+
+/*
+ * bf_vec_philox4x64_10 -- host-side evaluation of the Philox4x64-10 block function
+ * the device sampler uses (Salmon et al., SC'11; reading R9): out = philox(ctr, key).
+ * Needs no GPU; lets the generator be checked against published known answers.
+ */
+bf_status_t bf_vec_philox4x64_10(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]);
+
+/* Human-readable name of a status code (static storage). */
+const char *bf_vec_status_string(bf_status_t status);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BFVEC_H */

@@ -1,0 +1,181 @@
+"""Python binding of the C ABI (include/bfvec.h) with the same names.
+
+torch is used only for device buffers and streams: every step of the filter
+runs in libbfvec's CUDA kernels. Tensors must be contiguous float32 on a CUDA
+device, planar (d, rows, W).
+"""
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BfVecError, check
+
+BF_W_ALIAS = 1
+BF_W_SMALL_Z = 2
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dev(t: torch.Tensor, shape, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32 \
+            or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def philox4x64_10(ctr, key):
+    """Host evaluation of the sampler's Philox4x64-10 block function (no GPU needed)."""
+    lib = _lib.load()
+    c = (ctypes.c_uint64 * 4)(*[int(x) & 0xFFFFFFFFFFFFFFFF for x in ctr])
+    k = (ctypes.c_uint64 * 2)(*[int(x) & 0xFFFFFFFFFFFFFFFF for x in key])
+    o = (ctypes.c_uint64 * 4)()
+    check(lib.bf_vec_philox4x64_10(c, k, o), "bf_vec_philox4x64_10")
+    return [int(v) for v in o]
+
+
+class Plan:
+    """bf_vec_plan(H, W, d, sigma_s, C, N, M, seed) and the calls on it."""
+
+    def __init__(self, H, W, d, sigma_s, C, N, M, seed, value_range=255.0):
+        self._lib = _lib.load()
+        C = np.ascontiguousarray(np.asarray(C, dtype=np.float64).reshape(d, d))
+        h = ctypes.c_void_p()
+        check(self._lib.bf_vec_plan(int(H), int(W), int(d), float(sigma_s),
+                                    C.ctypes.data_as(ctypes.c_void_p), int(N), int(M),
+                                    ctypes.c_uint64(int(seed)), ctypes.byref(h)), "bf_vec_plan")
+        self._h = h
+        self.H, self.W, self.d, self.N, self.M = int(H), int(W), int(d), int(N), int(M)
+        self.sigma_s, self.seed = float(sigma_s), int(seed)
+        self.set_option("value_range", value_range)
+
+    # -- lifecycle ---------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.bf_vec_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- options / info ----------------------------------------------------
+    def set_option(self, name, value):
+        check(self._lib.bf_vec_set_option(self._h, name.encode(), float(value)), "bf_vec_set_option")
+
+    def info(self, name):
+        v = ctypes.c_longlong()
+        check(self._lib.bf_vec_plan_info(self._h, name.encode(), ctypes.byref(v)), "bf_vec_plan_info")
+        return int(v.value)
+
+    # -- sampler -----------------------------------------------------------
+    def sample_freqs(self, stream=None):
+        check(self._lib.bf_vec_sample_freqs(self._h, _stream_ptr(stream)), "bf_vec_sample_freqs")
+        return self
+
+    def get_draws(self, with_samples=True):
+        """(X (M,d) int32, t (M,d) float32, Q (d,d), alpha (d)); X and t are None
+        if with_samples is False (works without a GPU)."""
+        d, M = self.d, self.M
+        Q = np.empty((d, d), dtype=np.float64)
+        a = np.empty(d, dtype=np.float64)
+        X = np.empty((M, d), dtype=np.int32) if with_samples else None
+        t = np.empty((M, d), dtype=np.float32) if with_samples else None
+        ptr = lambda arr: arr.ctypes.data_as(ctypes.c_void_p) if arr is not None else None
+        check(self._lib.bf_vec_get_draws(self._h, ptr(X), ptr(t), ptr(Q), ptr(a)), "bf_vec_get_draws")
+        return X, t, Q, a
+
+    # -- filters -----------------------------------------------------------
+    def filter(self, f, out=None, stream=None):
+        shp = (self.d, self.H, self.W)
+        if out is None:
+            out = torch.empty(shp, dtype=torch.float32, device=f.device)
+        self.last_status = check(self._lib.bf_vec_filter(self._h, _dev(f, shp, "f"), _dev(out, shp, "out"),
+                                                         _stream_ptr(stream)), "bf_vec_filter")
+        return out
+
+    def filter_host(self, f_host, out_host=None, stream=None):
+        """bf_vec_filter_host: host (pinned) tensors in and out; synchronous."""
+        shp = (self.d, self.H, self.W)
+        if out_host is None:
+            out_host = torch.empty(shp, dtype=torch.float32, pin_memory=True)
+        for t, n in ((f_host, "f_host"), (out_host, "out_host")):
+            if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous() or tuple(t.shape) != shp:
+                raise ValueError(f"{n} must be a contiguous float32 host tensor of shape {shp}")
+        self.last_status = check(self._lib.bf_vec_filter_host(
+            self._h, ctypes.c_void_p(f_host.data_ptr()), ctypes.c_void_p(out_host.data_ptr()),
+            _stream_ptr(stream)), "bf_vec_filter_host")
+        return out_host
+
+    def filter_partial(self, f, k0, k1, PZ=None, rows_per_band=None, stream=None):
+        rpb = self.H if rows_per_band is None else int(rows_per_band)
+        n = (self.d + 1) * self.H * self.W
+        if PZ is None:
+            PZ = torch.empty(n, dtype=torch.float32, device=f.device)
+        check(self._lib.bf_vec_filter_partial(self._h, _dev(f, (self.d, self.H, self.W), "f"), int(k0), int(k1),
+                                              _dev(PZ, (PZ.numel(),), "PZ") if PZ.dim() == 1 else
+                                              _dev(PZ, tuple(PZ.shape), "PZ"), rpb, _stream_ptr(stream)),
+              "bf_vec_filter_partial")
+        if PZ.numel() != n:
+            raise ValueError("PZ must hold (d+1)*H*W floats")
+        return PZ
+
+    def normalize(self, PZ_band, row0, row1, out=None, stream=None):
+        rows = int(row1) - int(row0)
+        if PZ_band.numel() != (self.d + 1) * rows * self.W:
+            raise ValueError("PZ_band must hold (d+1)*(row1-row0)*W floats")
+        if out is None:
+            out = torch.empty((self.d, rows, self.W), dtype=torch.float32, device=PZ_band.device)
+        check(self._lib.bf_vec_normalize(self._h, _dev(PZ_band, tuple(PZ_band.shape), "PZ_band"), int(row0),
+                                         int(row1), _dev(out, (self.d, rows, self.W), "out"),
+                                         _stream_ptr(stream)), "bf_vec_normalize")
+        return out
+
+    def filter_rows(self, slab, slab_row0, row0, row1, out=None, stream=None):
+        rows = int(row1) - int(row0)
+        slab_rows = slab.shape[1]
+        if out is None:
+            out = torch.empty((self.d, rows, self.W), dtype=torch.float32, device=slab.device)
+        self.last_status = check(self._lib.bf_vec_filter_rows(
+            self._h, _dev(slab, (self.d, slab_rows, self.W), "slab"), int(slab_row0), int(slab_rows),
+            int(row0), int(row1), _dev(out, (self.d, rows, self.W), "out"), _stream_ptr(stream)),
+            "bf_vec_filter_rows")
+        return out
+
+    def direct(self, f, out=None, stream=None):
+        shp = (self.d, self.H, self.W)
+        if out is None:
+            out = torch.empty(shp, dtype=torch.float32, device=f.device)
+        check(self._lib.bf_vec_direct(self._h, _dev(f, shp, "f"), _dev(out, shp, "out"), _stream_ptr(stream)),
+              "bf_vec_direct")
+        return out
+
+    def diag(self):
+        zm = ctypes.c_float()
+        n = ctypes.c_longlong()
+        check(self._lib.bf_vec_diag(self._h, ctypes.byref(zm), ctypes.byref(n)), "bf_vec_diag")
+        return float(zm.value), int(n.value)
+
+
+def plan_for_config(cfg):
+    """Plan for a workloads.Config (BASELINE.json configs)."""
+    return Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, cfg.M, cfg.seed,
+                value_range=cfg.value_range)
+
+
+__all__ = ["Plan", "BfVecError", "philox4x64_10", "plan_for_config", "BF_W_ALIAS", "BF_W_SMALL_Z"]

@@ -1,0 +1,114 @@
+// internal.h -- private declarations of libbfvec (not part of the C ABI).
+// Nothing here is shared with oracle/: the two implementations are independent.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bfvec.h"
+
+namespace bfvec {
+
+constexpr int kMaxD = 8;
+constexpr int kMaxR = 64;
+constexpr int kTX = 32;            // output columns per strip (one warp of lanes)
+
+// Arguments of the fused MCSF kernel (one launch = one output band, one sample range).
+// Passed by value as a __grid_constant__ parameter, so the taps w[] become
+// constant-bank operands of the FFMAs.
+struct FusedArgs {
+    const float *f;       // planar (D, slab_rows, W) image slab (device)
+    long long plane;      // slab_rows * W
+    int d;                // image channels (<= compiled D; channels d..D-1 are zero)
+    int H, W;             // full image size (reflection is about the full image)
+    int slab_row0;        // image row of slab row 0
+    int slab_rows;        // rows present in the slab (reads are clamped to them)
+    int out_row0;         // first output row (image coordinates)
+    int out_rows;         // number of output rows
+    int tile_rows;        // rows per CTA tile (multiple of the kernel's KB)
+    int groups;           // sample groups (grid.z)
+    int k0, k1;           // sample range
+    const float *t;       // (M, d) frequency table, fp32
+    float *pz;            // (groups, D+1, out_rows, W): planes 0..D-1 = P' (centred), D = Z
+    float mu[kMaxD];      // centring offsets (exact invariance S[f-mu]+mu = S[f], reading R12)
+    float w[kMaxR + 1];   // normalised taps w[|m|], zero beyond the plan radius
+};
+
+struct KernelInfo {
+    int D, R;             // compiled vector dim and radius (taps beyond r are zero)
+    int threads;
+    int kb;               // output rows per chunk
+    size_t smem;
+    int regs;
+    int occupancy;        // CTAs per SM (from the occupancy API)
+};
+
+// Kernel-set dispatch (mcsf_fused.cu). Returns false if no instance fits.
+bool fused_select(int d, int r, KernelInfo *info);
+cudaError_t fused_launch(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s);
+
+// Sampler (sampler.cu)
+cudaError_t launch_sampler(int M, int d, int N, uint64_t seed, const double *dQ,
+                           const double *dgamma, int32_t *dX, float *dt, cudaStream_t s);
+void philox4x64_10_host(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]);
+
+// Epilogues (normalize.cu)
+cudaError_t launch_normalize_groups(const float *pz, int groups, int D, int d, int rows, int W,
+                                    const float *mu, float *out, float *diag, float inv_m,
+                                    float z_floor, cudaStream_t s);
+cudaError_t launch_finalize_partial(const float *pz, int groups, int D, int d, int rows, int W,
+                                    const float *mu, int rows_per_band, float *PZ, cudaStream_t s);
+cudaError_t launch_normalize_raw(const float *PZ, int d, int rows, int W, float *out, float *diag,
+                                 float inv_m, float z_floor, cudaStream_t s);
+cudaError_t launch_diag_reset(float *diag, cudaStream_t s);
+
+// Direct filter (direct.cu)
+cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const float *w,
+                          const float *A /* d x d: diag(alpha) Q^T scaled */, float *U,
+                          float *out, cudaStream_t s);
+
+}  // namespace bfvec
+
+struct bf_vec_plan_s {
+    int H, W, d, N, M, r;
+    double sigma_s;
+    uint64_t seed;
+    double C[64];
+    double Q[64];         // row-major, columns are eigenvectors q_k
+    double alpha[8];
+    float taps[bfvec::kMaxR + 1];
+    bool alias;           // static alias warning (BF_W_ALIAS)
+    // options
+    double z_floor = 0.05;
+    double value_range = 255.0;
+    int force_tile_rows = 0;
+    int force_groups = 0;
+    // device state (lazily created)
+    int device = -1;
+    bool sampled = false;
+    bfvec::KernelInfo kinfo{};
+    bool kinfo_ok = false;
+    int32_t *dX = nullptr;
+    float *dt = nullptr;
+    double *dQ = nullptr, *dgamma = nullptr;
+    float *dpz = nullptr;
+    size_t pz_bytes = 0;
+    float *ddiag = nullptr;     // [0] z_min (ordered-int encoded), [1] count
+    float *dU = nullptr;        // direct-filter scratch
+    size_t dU_bytes = 0;
+    float *dhost_in = nullptr, *dhost_out = nullptr;
+    size_t dhost_bytes = 0;
+    float mu[8];
+    cudaStream_t last = nullptr;
+    // last schedule
+    int last_tile_rows = 0, last_groups = 0;
+    long long last_ctas = 0;
+    int last_launches = 0;
+    // optional event timing of the fused kernel (option "profile")
+    bool profile = false;
+    static constexpr int kEvRing = 256;
+    cudaEvent_t ev[kEvRing][2] = {};
+    int ev_head = 0, ev_count = 0;   // pending event pairs (not yet folded into the total)
+    double fused_ms_total = 0.0;
+    long long fused_calls = 0;
+};

@@ -1,0 +1,552 @@
+// plan.cu -- host side of libbfvec: the C ABI (include/bfvec.h), Algorithm 1 setup
+// (L210-214), scheduling of the fused kernel, and the
+// orchestration of the device kernels on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "internal.h"
+
+using namespace bfvec;
+
+namespace {
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// Eq. (4): C = Q diag(1/alpha^2) Q^T by cyclic Jacobi rotations
+// in fp64, canonical order and signs of reading R8.
+// ---------------------------------------------------------------------------
+void jacobi_eig(int n, const double *Ain, double *evals, double *V) {
+    double A[64];
+    std::memcpy(A, Ain, sizeof(double) * n * n);
+    for (int i = 0; i < n * n; ++i) V[i] = 0.0;
+    for (int i = 0; i < n; ++i) V[i * n + i] = 1.0;
+    double frob = 0.0;
+    for (int i = 0; i < n * n; ++i) frob += A[i] * A[i];
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) off += A[p * n + q] * A[p * n + q];
+        if (off <= 1e-32 * frob) break;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                const double apq = A[p * n + q];
+                if (std::fabs(apq) < 1e-300) continue;
+                const double theta = (A[q * n + q] - A[p * n + p]) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < n; ++k) {
+                    const double akp = A[k * n + p], akq = A[k * n + q];
+                    A[k * n + p] = c * akp - s * akq;
+                    A[k * n + q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < n; ++k) {
+                    const double apk = A[p * n + k], aqk = A[q * n + k];
+                    A[p * n + k] = c * apk - s * aqk;
+                    A[q * n + k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < n; ++k) {
+                    const double vkp = V[k * n + p], vkq = V[k * n + q];
+                    V[k * n + p] = c * vkp - s * vkq;
+                    V[k * n + q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    for (int i = 0; i < n; ++i) evals[i] = A[i * n + i];
+}
+
+bf_status_t diagonalize(int d, const double *C, double *Q, double *alpha) {
+    double cmax = 0.0;
+    for (int i = 0; i < d * d; ++i) {
+        if (!std::isfinite(C[i])) return BF_E_ARG;
+        cmax = std::max(cmax, std::fabs(C[i]));
+    }
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j)
+            if (std::fabs(C[i * d + j] - C[j * d + i]) > 1e-12 * std::max(1.0, cmax)) return BF_E_NOT_SYMMETRIC;
+    bool diag = true;
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j)
+            if (i != j && C[i * d + j] != 0.0) diag = false;
+    double lam[8];
+    if (diag) {  // reading R8 (i): Q = I, no reordering
+        double lmax = 0.0;
+        for (int i = 0; i < d; ++i) lmax = std::max(lmax, C[i * d + i]);
+        for (int i = 0; i < d; ++i) {
+            if (!(C[i * d + i] > 1e-12 * lmax)) return BF_E_NOT_POSDEF;
+            alpha[i] = 1.0 / std::sqrt(C[i * d + i]);
+        }
+        for (int i = 0; i < d * d; ++i) Q[i] = 0.0;
+        for (int i = 0; i < d; ++i) Q[i * d + i] = 1.0;
+        return BF_OK;
+    }
+    double V[64];
+    jacobi_eig(d, C, lam, V);
+    double lmax = 0.0;
+    for (int i = 0; i < d; ++i) lmax = std::max(lmax, lam[i]);
+    for (int i = 0; i < d; ++i)
+        if (!(lam[i] > 1e-12 * lmax)) return BF_E_NOT_POSDEF;
+    // reading R8 (ii): C-eigenvalues ascending (alpha descending), stable
+    int order[8];
+    for (int i = 0; i < d; ++i) order[i] = i;
+    std::stable_sort(order, order + d, [&](int a, int b) { return lam[a] < lam[b]; });
+    for (int k = 0; k < d; ++k) {
+        const int src = order[k];
+        double mx = 0.0;
+        for (int r = 0; r < d; ++r) mx = std::max(mx, std::fabs(V[r * d + src]));
+        double sgn = 1.0;
+        for (int r = 0; r < d; ++r)
+            if (std::fabs(V[r * d + src]) > 1e-6 * mx) { sgn = V[r * d + src] < 0 ? -1.0 : 1.0; break; }
+        for (int r = 0; r < d; ++r) Q[r * d + k] = sgn * V[r * d + src];
+        alpha[k] = 1.0 / std::sqrt(lam[src]);
+    }
+    return BF_OK;
+}
+
+bf_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? BF_OK : BF_E_CUDA; }
+
+#define BF_CUDA(call)                                        \
+    do {                                                     \
+        cudaError_t _e = (call);                             \
+        if (_e != cudaSuccess) return BF_E_CUDA;             \
+    } while (0)
+
+bf_status_t ensure_device(bf_vec_plan_t p) {
+    if (p->device >= 0) return BF_OK;
+    int dev = 0;
+    BF_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    BF_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10) return BF_E_CUDA;  // sm_100a code only; no fallback
+    BF_CUDA(cudaMalloc(&p->dX, sizeof(int32_t) * (size_t)p->M * p->d));
+    BF_CUDA(cudaMalloc(&p->dt, sizeof(float) * (size_t)p->M * p->d));
+    BF_CUDA(cudaMalloc(&p->dQ, sizeof(double) * 64));
+    BF_CUDA(cudaMalloc(&p->dgamma, sizeof(double) * 8));
+    BF_CUDA(cudaMalloc(&p->ddiag, 16));
+    if (!fused_select(p->d, p->r, &p->kinfo)) return BF_E_UNSUPPORTED;
+    p->kinfo_ok = true;
+    p->device = dev;
+    return BF_OK;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// Choose (tile_rows, groups) for one fused launch by a simple cost model:
+// per CTA time ~ samples x (H-pass rows + V-pass rows + per-chunk overhead),
+// whole launch ~ waves x CTA time + the partial-sum traffic of G groups.
+void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows, int *groups) {
+    const KernelInfo &ki = p->kinfo;
+    const int KB = ki.kb, R = ki.R, D = ki.D;
+    const int nx = (p->W + kTX - 1) / kTX;
+    const int occ = std::max(1, ki.occupancy);
+    const long long slots = (long long)sm_count() * occ;
+    // seconds per "row unit" (one 32-column row of one pass for all channels) per CTA
+    const double row_unit = 32.0 * 2.0 * (D + 1) * (2 * R + 1) / (128.0 / occ) / 1.9e9 / 0.6;
+    const double chunk_overhead_rows = 4.0;
+    double best = 1e300;
+    int bt = KB, bg = 1;
+    const int rmax = (out_rows + KB - 1) / KB * KB;
+    for (int ty = KB;; ty *= 2) {
+        const int t = std::min(ty, rmax);
+        // keep the concurrently updated partial tiles L2-resident (~64 MB)
+        const double ws = (double)slots * 32.0 * t * (D + 1) * 4.0;
+        const int ny = (out_rows + t - 1) / t;
+        const int chunks = (std::min(t, out_rows) + KB - 1) / KB;
+        for (int G = 1; G <= std::min(ns, 256); ++G) {
+            const long long ctas = (long long)nx * ny * G;
+            if (ctas > 2147483647LL / 2) continue;
+            const int mg = (ns + G - 1) / G;
+            const double cta = mg * (2.0 * chunks * KB + 2.0 * R + chunks * chunk_overhead_rows) * row_unit;
+            const long long waves = (ctas + slots - 1) / slots;
+            double tt = waves * cta;
+            if (G > 1) tt += (double)G * (D + 1) * out_rows * (double)p->W * 4.0 * 2.0 / 5e12;
+            if (ws > 64e6) tt *= 1.15;
+            if (tt < best * 0.999) { best = tt; bt = t; bg = G; }
+        }
+        if (ty >= rmax) break;
+    }
+    if (p->force_tile_rows > 0) bt = (p->force_tile_rows + KB - 1) / KB * KB;
+    if (p->force_groups > 0) bg = std::min(p->force_groups, ns);
+    *tile_rows = bt;
+    *groups = bg;
+}
+
+bf_status_t ensure_pz(bf_vec_plan_t p, size_t bytes) {
+    if (p->pz_bytes >= bytes) return BF_OK;
+    if (p->dpz) cudaFree(p->dpz);
+    p->dpz = nullptr;
+    p->pz_bytes = 0;
+    BF_CUDA(cudaMalloc(&p->dpz, bytes));
+    p->pz_bytes = bytes;
+    return BF_OK;
+}
+
+void fill_mu(bf_vec_plan_t p) {
+    for (int c = 0; c < 8; ++c) p->mu[c] = (c < p->d) ? (float)(0.5 * p->value_range) : 0.f;
+}
+
+// fold every pending fused-launch event interval into the running total
+void collect_profile(bf_vec_plan_t p) {
+    while (p->ev_count > 0) {
+        const int i = (p->ev_head - p->ev_count + bf_vec_plan_s::kEvRing) % bf_vec_plan_s::kEvRing;
+        float ms = 0.f;
+        if (cudaEventSynchronize(p->ev[i][1]) == cudaSuccess &&
+            cudaEventElapsedTime(&ms, p->ev[i][0], p->ev[i][1]) == cudaSuccess) {
+            p->fused_ms_total += ms;
+            p->fused_calls += 1;
+        }
+        p->ev_count -= 1;
+    }
+}
+
+// one fused launch: output rows [out_row0, out_row0+out_rows), samples [k0, k1)
+bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_row0, int out_row0,
+                      int out_rows, int k0, int k1, cudaStream_t s, int *groups_out) {
+    int tile_rows = 0, groups = 1;
+    choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups);
+    const KernelInfo &ki = p->kinfo;
+    const size_t need = sizeof(float) * (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;
+    bf_status_t st = ensure_pz(p, need);
+    if (st != BF_OK) return st;
+    FusedArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.f = f;
+    a.plane = (long long)slab_rows * p->W;
+    a.slab_rows = slab_rows;
+    a.d = p->d;
+    a.H = p->H;
+    a.W = p->W;
+    a.slab_row0 = slab_row0;
+    a.out_row0 = out_row0;
+    a.out_rows = out_rows;
+    a.tile_rows = tile_rows;
+    a.groups = groups;
+    a.k0 = k0;
+    a.k1 = k1;
+    a.t = p->dt;
+    a.pz = p->dpz;
+    fill_mu(p);
+    for (int c = 0; c < kMaxD; ++c) a.mu[c] = p->mu[c];
+    for (int i = 0; i <= kMaxR; ++i) a.w[i] = (i <= p->r) ? p->taps[i] : 0.f;
+    dim3 grid((p->W + kTX - 1) / kTX, (out_rows + tile_rows - 1) / tile_rows, groups);
+    p->last_tile_rows = tile_rows;
+    p->last_groups = groups;
+    p->last_ctas = (long long)grid.x * grid.y * grid.z;
+    int slot = -1;
+    if (p->profile) {
+        if (p->ev_count == bf_vec_plan_s::kEvRing) collect_profile(p);
+        slot = p->ev_head;
+        for (int j = 0; j < 2; ++j)
+            if (!p->ev[slot][j]) BF_CUDA(cudaEventCreate(&p->ev[slot][j]));
+        BF_CUDA(cudaEventRecord(p->ev[slot][0], s));
+    }
+    BF_CUDA(fused_launch(ki, a, grid, s));
+    if (slot >= 0) {
+        BF_CUDA(cudaEventRecord(p->ev[slot][1], s));
+        p->ev_head = (p->ev_head + 1) % bf_vec_plan_s::kEvRing;
+        p->ev_count += 1;
+    }
+    *groups_out = groups;
+    return BF_OK;
+}
+
+bool valid_plan(bf_vec_plan_t p) { return p != nullptr; }
+
+}  // namespace
+
+extern "C" {
+
+const char *bf_vec_status_string(bf_status_t st) {
+    switch (st) {
+        case BF_OK: return "BF_OK";
+        case BF_E_ARG: return "BF_E_ARG: invalid argument";
+        case BF_E_NOT_SYMMETRIC: return "BF_E_NOT_SYMMETRIC: covariance not symmetric";
+        case BF_E_NOT_POSDEF: return "BF_E_NOT_POSDEF: covariance not positive definite";
+        case BF_E_UNSUPPORTED: return "BF_E_UNSUPPORTED: configuration outside the compiled kernel set";
+        case BF_E_CUDA: return "BF_E_CUDA: CUDA error or no sm_100 device";
+        case BF_E_STATE: return "BF_E_STATE: call order violated";
+        case BF_W_ALIAS: return "BF_W_ALIAS: raised cosine leaves its main lobe on the data range";
+        case BF_W_SMALL_Z: return "BF_W_SMALL_Z: some pixels have Z/M below z_floor";
+    }
+    return "unknown status";
+}
+
+bf_status_t bf_vec_plan(int H, int W, int d, double sigma_s, const double *C, int N, int M,
+                        uint64_t seed, bf_vec_plan_t *out) {
+    if (!out || !C) return BF_E_ARG;
+    *out = nullptr;
+    if (H < 1 || W < 1 || d < 1 || d > kMaxD || M < 1) return BF_E_ARG;
+    if (!(sigma_s > 0.0) || !std::isfinite(sigma_s)) return BF_E_ARG;
+    if (N < 2 || N > 64 || (N & 1)) return BF_E_ARG;
+    const int r = (int)std::ceil(3.0 * sigma_s - 1e-12);   // reading R2
+    if (r < 1 || r > kMaxR) return BF_E_ARG;
+    bf_vec_plan_t p = new (std::nothrow) bf_vec_plan_s();
+    if (!p) return BF_E_ARG;
+    p->H = H; p->W = W; p->d = d; p->N = N; p->M = M; p->r = r;
+    p->sigma_s = sigma_s;
+    p->seed = seed;
+    std::memcpy(p->C, C, sizeof(double) * d * d);
+    bf_status_t st = diagonalize(d, C, p->Q, p->alpha);
+    if (st != BF_OK) { delete p; return st; }
+    // Eq. (1) spatial taps, normalised in fp64 (reading R3), rounded once to fp32
+    double w[kMaxR + 1], sum = 0.0;
+    for (int m = 0; m <= r; ++m) {
+        w[m] = std::exp(-(double)m * m / (2.0 * sigma_s * sigma_s));
+        sum += (m == 0 ? 1.0 : 2.0) * w[m];
+    }
+    for (int m = 0; m <= kMaxR; ++m) p->taps[m] = (m <= r) ? (float)(w[m] / sum) : 0.f;
+    // alias warning (reading R14): (pi/2) sqrt(N) < alpha_c R ||q_c||_1
+    p->alias = false;
+    for (int c = 0; c < d; ++c) {
+        double l1 = 0.0;
+        for (int rr = 0; rr < d; ++rr) l1 += std::fabs(p->Q[rr * d + c]);
+        if (0.5 * M_PI * std::sqrt((double)N) < p->alpha[c] * p->value_range * l1) p->alias = true;
+    }
+    fill_mu(p);
+    *out = p;
+    return BF_OK;
+}
+
+void bf_vec_plan_destroy(bf_vec_plan_t p) {
+    if (!p) return;
+    if (p->device >= 0) {
+        if (p->last) cudaStreamSynchronize(p->last);
+        cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
+        cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU);
+        cudaFree(p->dhost_in); cudaFree(p->dhost_out);
+        for (auto &pair : p->ev)
+            for (auto &e : pair)
+                if (e) cudaEventDestroy(e);
+    }
+    delete p;
+}
+
+bf_status_t bf_vec_sample_freqs(bf_vec_plan_t p, void *stream) {
+    if (!valid_plan(p)) return BF_E_ARG;
+    bf_status_t st = ensure_device(p);
+    if (st != BF_OK) return st;
+    double gamma[8];
+    for (int c = 0; c < p->d; ++c) gamma[c] = p->alpha[c] / std::sqrt((double)p->N);
+    BF_CUDA(cudaMemcpy(p->dQ, p->Q, sizeof(double) * p->d * p->d, cudaMemcpyHostToDevice));
+    BF_CUDA(cudaMemcpy(p->dgamma, gamma, sizeof(double) * p->d, cudaMemcpyHostToDevice));
+    BF_CUDA(launch_sampler(p->M, p->d, p->N, p->seed, p->dQ, p->dgamma, p->dX, p->dt, S(stream)));
+    p->sampled = true;
+    p->last = S(stream);
+    return BF_OK;
+}
+
+bf_status_t bf_vec_get_draws(bf_vec_plan_t p, int32_t *X, float *t, double *Q, double *alpha) {
+    if (!valid_plan(p)) return BF_E_ARG;
+    if (Q) std::memcpy(Q, p->Q, sizeof(double) * p->d * p->d);
+    if (alpha) std::memcpy(alpha, p->alpha, sizeof(double) * p->d);
+    if (X || t) {
+        if (!p->sampled) return BF_E_STATE;
+        BF_CUDA(cudaStreamSynchronize(p->last));
+        if (X) BF_CUDA(cudaMemcpy(X, p->dX, sizeof(int32_t) * (size_t)p->M * p->d, cudaMemcpyDeviceToHost));
+        if (t) BF_CUDA(cudaMemcpy(t, p->dt, sizeof(float) * (size_t)p->M * p->d, cudaMemcpyDeviceToHost));
+    }
+    return BF_OK;
+}
+
+static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows, int slab_row0,
+                               int row0, int row1, float *out, cudaStream_t s) {
+    if (!p->sampled) return BF_E_STATE;
+    int groups = 1;
+    bf_status_t st = run_fused(p, slab, slab_rows, slab_row0, row0, row1 - row0, 0, p->M, s, &groups);
+    if (st != BF_OK) return st;
+    BF_CUDA(launch_diag_reset(p->ddiag, s));
+    BF_CUDA(launch_normalize_groups(p->dpz, groups, p->kinfo.D, p->d, row1 - row0, p->W, p->mu, out,
+                                    p->ddiag, 1.0f / p->M, (float)p->z_floor, s));
+    p->last_launches = 3;
+    p->last = s;
+    return p->alias ? BF_W_ALIAS : BF_OK;
+}
+
+bf_status_t bf_vec_filter(bf_vec_plan_t p, const float *f, float *out, void *stream) {
+    if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
+    if (p->device < 0) return BF_E_STATE;
+    return filter_band(p, f, p->H, 0, 0, p->H, out, S(stream));
+}
+
+bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {
+    if (!valid_plan(p) || !f_host || !out_host) return BF_E_ARG;
+    if (p->device < 0) return BF_E_STATE;
+    const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
+    if (p->dhost_bytes < bytes) {
+        cudaFree(p->dhost_in); cudaFree(p->dhost_out);
+        p->dhost_in = p->dhost_out = nullptr;
+        p->dhost_bytes = 0;
+        BF_CUDA(cudaMalloc(&p->dhost_in, bytes));
+        BF_CUDA(cudaMalloc(&p->dhost_out, bytes));
+        p->dhost_bytes = bytes;
+    }
+    cudaStream_t s = S(stream);
+    BF_CUDA(cudaMemcpyAsync(p->dhost_in, f_host, bytes, cudaMemcpyHostToDevice, s));
+    bf_status_t st = filter_band(p, p->dhost_in, p->H, 0, 0, p->H, p->dhost_out, s);
+    if (st < 0) return st;
+    BF_CUDA(cudaMemcpyAsync(out_host, p->dhost_out, bytes, cudaMemcpyDeviceToHost, s));
+    BF_CUDA(cudaStreamSynchronize(s));
+    return st;
+}
+
+bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k1, float *PZ,
+                                  int rows_per_band, void *stream) {
+    if (!valid_plan(p) || !f || !PZ) return BF_E_ARG;
+    if (k0 < 0 || k1 > p->M || k0 > k1 || rows_per_band < 1 || rows_per_band > p->H) return BF_E_ARG;
+    if (p->device < 0 || !p->sampled) return BF_E_STATE;
+    cudaStream_t s = S(stream);
+    if (k0 == k1) {
+        BF_CUDA(cudaMemsetAsync(PZ, 0, sizeof(float) * (size_t)(p->d + 1) * p->H * p->W, s));
+        return BF_OK;
+    }
+    int groups = 1;
+    bf_status_t st = run_fused(p, f, p->H, 0, 0, p->H, k0, k1, s, &groups);
+    if (st != BF_OK) return st;
+    BF_CUDA(launch_finalize_partial(p->dpz, groups, p->kinfo.D, p->d, p->H, p->W, p->mu, rows_per_band, PZ, s));
+    p->last_launches = 2;
+    p->last = s;
+    return BF_OK;
+}
+
+bf_status_t bf_vec_normalize(bf_vec_plan_t p, const float *PZ_band, int row0, int row1, float *out_band,
+                             void *stream) {
+    if (!valid_plan(p) || !PZ_band || !out_band) return BF_E_ARG;
+    if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
+    bf_status_t st = ensure_device(p);
+    if (st != BF_OK) return st;
+    cudaStream_t s = S(stream);
+    BF_CUDA(launch_diag_reset(p->ddiag, s));
+    BF_CUDA(launch_normalize_raw(PZ_band, p->d, row1 - row0, p->W, out_band, p->ddiag, 1.0f / p->M,
+                                 (float)p->z_floor, s));
+    p->last_launches = 2;
+    p->last = s;
+    return BF_OK;
+}
+
+bf_status_t bf_vec_filter_rows(bf_vec_plan_t p, const float *slab, int slab_row0, int slab_rows, int row0,
+                               int row1, float *out_band, void *stream) {
+    if (!valid_plan(p) || !slab || !out_band) return BF_E_ARG;
+    if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
+    if (slab_row0 < 0 || slab_rows < 1 || slab_row0 + slab_rows > p->H) return BF_E_ARG;
+    if (p->device < 0) return BF_E_STATE;
+    // every reflected row within r of the band must be in the slab (rows the
+    // compiled radius reads beyond r carry zero taps and are clamped in-kernel)
+    for (long long y = (long long)row0 - p->r; y < (long long)row1 + p->r; ++y) {
+        const long long n = p->H, q = 2 * n;
+        long long i = y % q;
+        if (i < 0) i += q;
+        const long long yr = i < n ? i : q - 1 - i;
+        if (yr < slab_row0 || yr >= slab_row0 + slab_rows) return BF_E_ARG;
+    }
+    return filter_band(p, slab, slab_rows, slab_row0, row0, row1, out_band, S(stream));
+}
+
+bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *stream) {
+    if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
+    bf_status_t st = ensure_device(p);
+    if (st != BF_OK) return st;
+    const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
+    if (p->dU_bytes < bytes) {
+        cudaFree(p->dU);
+        p->dU = nullptr;
+        p->dU_bytes = 0;
+        BF_CUDA(cudaMalloc(&p->dU, bytes));
+        p->dU_bytes = bytes;
+    }
+    // A = sqrt(log2(e)/2) diag(alpha) Q^T  (Eq. (4)): |A (f_j - f_i)|^2 = log2(e) x^T C^-1 x / 2
+    float A[64];
+    const double sc = std::sqrt(0.5 / std::log(2.0));
+    for (int k = 0; k < p->d; ++k)
+        for (int c = 0; c < p->d; ++c) A[k * p->d + c] = (float)(sc * p->alpha[k] * p->Q[c * p->d + k]);
+    cudaStream_t s = S(stream);
+    BF_CUDA(launch_direct(f, p->d, p->H, p->W, p->r, p->taps, A, p->dU, out, s));
+    p->last_launches = 2;
+    p->last = s;
+    return BF_OK;
+}
+
+bf_status_t bf_vec_diag(bf_vec_plan_t p, float *z_min, long long *n_small_z) {
+    if (!valid_plan(p)) return BF_E_ARG;
+    if (p->device < 0) return BF_E_STATE;
+    BF_CUDA(cudaStreamSynchronize(p->last));
+    unsigned long long h[2];
+    BF_CUDA(cudaMemcpy(h, p->ddiag, 16, cudaMemcpyDeviceToHost));
+    const unsigned int key = (unsigned int)(h[0] & 0xFFFFFFFFull);
+    unsigned int u = (key & 0x80000000u) ? (key & 0x7FFFFFFFu) : ~key;
+    float zm;
+    std::memcpy(&zm, &u, 4);
+    if (key == 0xFFFFFFFFu) zm = NAN;
+    if (z_min) *z_min = zm;
+    if (n_small_z) *n_small_z = (long long)h[1];
+    return h[1] ? BF_W_SMALL_Z : BF_OK;
+}
+
+bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
+    if (!valid_plan(p) || !name) return BF_E_ARG;
+    if (!std::strcmp(name, "z_floor")) { p->z_floor = v; return BF_OK; }
+    if (!std::strcmp(name, "value_range")) {
+        if (!(v > 0) || !std::isfinite(v)) return BF_E_ARG;
+        p->value_range = v;
+        fill_mu(p);
+        p->alias = false;
+        for (int c = 0; c < p->d; ++c) {
+            double l1 = 0.0;
+            for (int rr = 0; rr < p->d; ++rr) l1 += std::fabs(p->Q[rr * p->d + c]);
+            if (0.5 * M_PI * std::sqrt((double)p->N) < p->alpha[c] * v * l1) p->alias = true;
+        }
+        return BF_OK;
+    }
+    if (!std::strcmp(name, "tile_rows")) { if (v < 0) return BF_E_ARG; p->force_tile_rows = (int)v; return BF_OK; }
+    if (!std::strcmp(name, "groups")) { if (v < 0) return BF_E_ARG; p->force_groups = (int)v; return BF_OK; }
+    if (!std::strcmp(name, "profile")) {
+        collect_profile(p);
+        p->profile = v != 0.0;
+        p->fused_ms_total = 0.0;
+        p->fused_calls = 0;
+        return BF_OK;
+    }
+    return BF_E_ARG;
+}
+
+bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value) {
+    if (!valid_plan(p) || !name || !value) return BF_E_ARG;
+    const KernelInfo &k = p->kinfo;
+    if (!std::strcmp(name, "fused_ns_total") || !std::strcmp(name, "fused_calls")) {
+        collect_profile(p);
+        *value = !std::strcmp(name, "fused_calls") ? p->fused_calls : (long long)(p->fused_ms_total * 1e6);
+        return BF_OK;
+    }
+    struct { const char *n; long long v; } tab[] = {
+        {"radius", p->r}, {"d", p->d}, {"H", p->H}, {"W", p->W}, {"M", p->M}, {"N", p->N},
+        {"tile_rows", p->last_tile_rows}, {"groups", p->last_groups}, {"ctas", p->last_ctas},
+        {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
+        {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
+        {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0},
+    };
+    for (auto &e : tab)
+        if (!std::strcmp(e.n, name)) { *value = e.v; return BF_OK; }
+    return BF_E_ARG;
+}
+
+bf_status_t bf_vec_philox4x64_10(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]) {
+    if (!ctr || !key || !out) return BF_E_ARG;
+    philox4x64_10_host(ctr, key, out);
+    return BF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol that
+include/bfvec.h declares, and its host-side logic (Philox block function,
+diagonalisation, validation) is right. No kernel is launched."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT, golden_lines
+
+HEADER = os.path.join(ROOT, "include", "bfvec.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bf_vec_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1605_02164_b200 import _lib
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    names = _declared()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.SIGNATURES)
+
+
+def test_philox_host_block_known_answers():
+    from paper_1605_02164_b200 import philox4x64_10
+    for ln in golden_lines("philox4x64_10_kat.txt"):
+        h = [int(x, 16) for x in ln.split()]
+        assert philox4x64_10(h[0:4], h[4:6]) == h[6:10]
+
+
+def test_philox_host_matches_numpy_stream():
+    from paper_1605_02164_b200 import philox4x64_10
+    seed = 4
+    words = [int(w) for w in np.random.Philox(key=seed).random_raw(12)]
+    for b in range(3):
+        assert philox4x64_10([b + 1, 0, 0, 0], [seed, 0]) == words[4 * b:4 * b + 4]
+
+
+@pytest.mark.parametrize("d,seed", [(2, 0), (3, 1), (5, 2), (8, 3)])
+def test_plan_diagonalisation_matches_oracle(d, seed):
+    from oracle import plan as oplan
+    from paper_1605_02164_b200 import Plan
+    rng = np.random.default_rng(seed)
+    A = rng.normal(size=(d, d))
+    C = 900.0 * (A @ A.T / d + np.eye(d))
+    p = Plan(32, 32, d, 1.0, C, 10, 4, 0)
+    _, _, Q, a = p.get_draws(with_samples=False)
+    Qo, ao = oplan.diagonalize(C)
+    np.testing.assert_allclose(a, ao, rtol=1e-12)
+    np.testing.assert_allclose(Q, Qo, atol=1e-10)
+
+
+def test_plan_validation_errors():
+    from paper_1605_02164_b200 import BfVecError, Plan
+    C = np.eye(3) * 100.0
+    for args in [(0, 8, 3, 1.0, C, 10, 4, 0), (8, 8, 3, 0.0, C, 10, 4, 0), (8, 8, 3, 1.0, C, 11, 4, 0),
+                 (8, 8, 3, 1.0, C, 10, 0, 0), (8, 8, 9, 1.0, np.eye(9), 10, 4, 0),
+                 (8, 8, 3, 30.0, C, 10, 4, 0)]:
+        with pytest.raises(BfVecError):
+            Plan(*args)
+    with pytest.raises(BfVecError) as e:
+        Plan(8, 8, 2, 1.0, np.array([[1.0, 0.5], [0.4, 1.0]]), 10, 4, 0)
+    assert e.value.status == -2
+    with pytest.raises(BfVecError) as e:
+        Plan(8, 8, 2, 1.0, np.array([[1.0, 2.0], [2.0, 1.0]]), 10, 4, 0)
+    assert e.value.status == -3
+
+
+def test_filter_requires_sampling_first():
+    torch = pytest.importorskip("torch")
+    from paper_1605_02164_b200 import BfVecError, Plan
+    p = Plan(8, 8, 3, 1.0, np.eye(3) * 100.0, 10, 4, 0)
+    with pytest.raises(BfVecError):
+        p.get_draws(with_samples=True)
+
+
+def test_alias_warning_static():
+    from paper_1605_02164_b200 import Plan
+    # alpha R = 255/30 = 8.5 > (pi/2) sqrt(4) = 3.14 -> aliasing; N = 40 -> 9.93 > 8.5: fine
+    assert Plan(8, 8, 1, 1.0, [[900.0]], 4, 4, 0).info("alias") == 1
+    assert Plan(8, 8, 1, 1.0, [[900.0]], 40, 4, 0).info("alias") == 0
