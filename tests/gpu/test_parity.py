@@ -72,7 +72,7 @@ def test_config_bands_parity(i):
     pix += [(0, 0), (cfg.H - 1, cfg.W - 1), (cfg.H // 2, 0), (0, cfg.W - 1)]
     S_o, P_o, Z_o = filters.mc_filter_pixels(get_rows, cfg.H, cfg.W, pix, Q, a, cfg.N, Y, cfg.sigma_s)
     ys, xs = np.array(pix).T
-    res = H.gates(cfg, S_g[:, ys, xs].T, P_g[:, ys, xs].T, Z_g[ys, xs], S_o, P_o, Z_o)
+    res = H.gates(cfg, S_g[:, ys, xs], P_g[:, ys, xs], Z_g[ys, xs], S_o.T, P_o.T, Z_o)
     print(f"config {i} pixels: {res}")
     H.assert_gates(res)
 
