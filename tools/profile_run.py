@@ -1,0 +1,37 @@
+"""Small driver for ncu captures: filters `--rows` output rows of config `--config`
+(band sharding entry, same fused kernel and schedule logic as the bench) `--reps` times."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from oracle import native  # noqa: E402  (slab bounds only)
+from paper_1605_02164_b200 import Plan  # noqa: E402
+from workloads import CONFIGS, make_image_rows  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=5)
+ap.add_argument("--rows", type=int, default=0)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--samples", type=int, default=0)
+a = ap.parse_args()
+cfg = CONFIGS[a.config]
+rows = a.rows or cfg.H
+y0 = (cfg.H - rows) // 2
+s0, s1 = native.slab_bounds(cfg.H, y0, rows, cfg.radius)
+M = a.samples or cfg.M
+p = Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, M, cfg.seed, value_range=cfg.value_range)
+p.sample_freqs()
+slab = torch.from_numpy(make_image_rows(cfg, s0, s1)).cuda()
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+for i in range(a.reps):
+    ev[0].record()
+    out = p.filter_rows(slab, s0, y0, y0 + rows)
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1])
+    print(f"rep {i}: {ms:.3f} ms  {rows * cfg.W * M / ms / 1e6:.3e} px*samples/s  "
+          f"tile_rows={p.info('tile_rows')} groups={p.info('groups')} ctas={p.info('ctas')}")
