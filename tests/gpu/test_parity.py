@@ -138,7 +138,8 @@ def test_forced_schedules_agree():
         S, P, Z = H.gpu_run(p, f)
         assert p.info("groups") == g
         np.testing.assert_allclose(Z, base[2], atol=1e-5 * cfg.M)
-        np.testing.assert_allclose(S, base[0], atol=2e-3)
+        ok = base[2] / cfg.M >= H.Z_FLOOR            # conditioned pixels (reading R5)
+        assert np.abs(S - base[0])[:, ok].max() < 2e-3
 
 
 def test_determinism_bitwise():
@@ -157,11 +158,13 @@ def test_filter_rows_band_equals_full():
     f = torch.from_numpy(f_np).cuda()
     p = H.gpu_plan(cfg)
     full = p.filter(f).cpu().numpy()
+    Z = p.filter_partial(f, 0, cfg.M).cpu().numpy().reshape(cfg.d + 1, cfg.H, cfg.W)[cfg.d]
     r = cfg.radius
     for (y0, y1) in [(0, 100), (200, 333), (480, 512)]:
         s0, s1 = native.slab_bounds(cfg.H, y0, y1 - y0, r)
         out = p.filter_rows(f[:, s0:s1].contiguous(), s0, y0, y1).cpu().numpy()
-        np.testing.assert_allclose(out, full[:, y0:y1], atol=2e-3)
+        ok = Z[y0:y1] / cfg.M >= H.Z_FLOOR           # conditioned pixels (reading R5)
+        assert np.abs(out - full[:, y0:y1])[:, ok].max() < 2e-3
 
 
 def test_sample_shards_sum_to_full():
