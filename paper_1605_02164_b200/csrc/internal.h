@@ -2,6 +2,7 @@
 // Nothing here is shared with oracle/: the two implementations are independent.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -15,29 +16,33 @@ constexpr int kTX = 32;            // output columns per strip (one warp of lane
 
 // Arguments of the fused MCSF kernel (one launch = one output band, one sample range).
 // Passed by value as a __grid_constant__ parameter, so the taps w[] become
-// constant-bank operands of the FFMAs.
-struct FusedArgs {
-    const float *f;       // planar (D, slab_rows, W) image slab (device)
-    long long plane;      // slab_rows * W
+// constant-bank / uniform-register operands of the FFMA2s and the tensor map is
+// addressable by the TMA unit.
+struct alignas(64) FusedArgs {
+    CUtensorMap tmap;     // 3-D map over the padded copy: dims {DP, Wp, Hp}, box {DP, WIN, SH}
     int d;                // image channels (<= compiled D; channels d..D-1 are zero)
-    int H, W;             // full image size (reflection is about the full image)
-    int slab_row0;        // image row of slab row 0
-    int slab_rows;        // rows present in the slab (reads are clamped to them)
-    int out_row0;         // first output row (image coordinates)
+    int W;                // image width
+    int out_row0;         // first output row (image coordinates); pad row 0 = out_row0 - R
     int out_rows;         // number of output rows
     int tile_rows;        // rows per CTA tile (multiple of the kernel's KB)
     int groups;           // sample groups (grid.z)
     int k0, k1;           // sample range
     const float *t;       // (M, d) frequency table, fp32
     float *pz;            // (groups, D+1, out_rows, W): planes 0..D-1 = P' (centred), D = Z
-    float mu[kMaxD];      // centring offsets (exact invariance S[f-mu]+mu = S[f], reading R12)
     float w[kMaxR + 1];   // normalised taps w[|m|], zero beyond the plan radius
+};
+
+struct PadMu {
+    float v[kMaxD];       // centring offsets (exact invariance S[f-mu]+mu = S[f], reading R12)
 };
 
 struct KernelInfo {
     int D, R;             // compiled vector dim and radius (taps beyond r are zero)
     int threads;
     int kb;               // output rows per chunk
+    int sh;               // rows per TMA box
+    int dp;               // floats per padded pixel
+    int win;              // haloed columns per box (32 + 2R)
     size_t smem;
     int regs;
     int occupancy;        // CTAs per SM (from the occupancy API)
@@ -46,6 +51,11 @@ struct KernelInfo {
 // Kernel-set dispatch (mcsf_fused.cu). Returns false if no instance fits.
 bool fused_select(int d, int r, KernelInfo *info);
 cudaError_t fused_launch(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s);
+
+// Reflect-padded, centred, interleaved copy of the input for the TMA loads (pad.cu)
+cudaError_t launch_pad(const float *f, long long plane, int d, int H, int W, int slab_row0, int slab_rows,
+                       int row_begin, int Hp, int Wp, int R, int DP, const float *mu, float *fpad,
+                       cudaStream_t s);
 
 // Sampler (sampler.cu)
 cudaError_t launch_sampler(int M, int d, int N, uint64_t seed, const double *dQ,
@@ -94,6 +104,8 @@ struct bf_vec_plan_s {
     float *dpz = nullptr;
     size_t pz_bytes = 0;
     float *ddiag = nullptr;     // [0] z_min (ordered-int encoded), [1] count
+    float *dfpad = nullptr;     // padded input copy (pad.cu), TMA source
+    size_t fpad_bytes = 0;
     float *dU = nullptr;        // direct-filter scratch
     size_t dU_bytes = 0;
     float *dhost_in = nullptr, *dhost_out = nullptr;

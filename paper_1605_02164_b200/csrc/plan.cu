@@ -214,6 +214,31 @@ void collect_profile(bf_vec_plan_t p) {
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bf_status_t encode_tmap(CUtensorMap *map, float *base, int dp, int Wp, int Hp, int win, int sh) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !ptr)
+            return BF_E_CUDA;
+        fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    const cuuint64_t dims[3] = {(cuuint64_t)dp, (cuuint64_t)Wp, (cuuint64_t)Hp};
+    const cuuint64_t strides[2] = {(cuuint64_t)dp * 4, (cuuint64_t)Wp * dp * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)dp, (cuuint32_t)win, (cuuint32_t)sh};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? BF_OK : BF_E_CUDA;
+}
+
 // one fused launch: output rows [out_row0, out_row0+out_rows), samples [k0, k1)
 bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_row0, int out_row0,
                       int out_rows, int k0, int k1, cudaStream_t s, int *groups_out) {
@@ -223,15 +248,26 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
     const size_t need = sizeof(float) * (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;
     bf_status_t st = ensure_pz(p, need);
     if (st != BF_OK) return st;
+    // reflect-padded, centred, interleaved copy of the rows this launch reads (pad.cu)
+    const int R = ki.R;
+    const int Hp = out_rows + 2 * R, Wp = p->W + 2 * R;
+    const size_t fbytes = sizeof(float) * (size_t)Hp * Wp * ki.dp;
+    if (p->fpad_bytes < fbytes) {
+        cudaFree(p->dfpad);
+        p->dfpad = nullptr;
+        p->fpad_bytes = 0;
+        BF_CUDA(cudaMalloc(&p->dfpad, fbytes));
+        p->fpad_bytes = fbytes;
+    }
+    fill_mu(p);
+    BF_CUDA(launch_pad(f, (long long)slab_rows * p->W, p->d, p->H, p->W, slab_row0, slab_rows, out_row0 - R, Hp, Wp,
+                       R, ki.dp, p->mu, p->dfpad, s));
     FusedArgs a;
     std::memset(&a, 0, sizeof(a));
-    a.f = f;
-    a.plane = (long long)slab_rows * p->W;
-    a.slab_rows = slab_rows;
+    st = encode_tmap(&a.tmap, p->dfpad, ki.dp, Wp, Hp, ki.win, ki.sh);
+    if (st != BF_OK) return st;
     a.d = p->d;
-    a.H = p->H;
     a.W = p->W;
-    a.slab_row0 = slab_row0;
     a.out_row0 = out_row0;
     a.out_rows = out_rows;
     a.tile_rows = tile_rows;
@@ -240,8 +276,6 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
     a.k1 = k1;
     a.t = p->dt;
     a.pz = p->dpz;
-    fill_mu(p);
-    for (int c = 0; c < kMaxD; ++c) a.mu[c] = p->mu[c];
     for (int i = 0; i <= kMaxR; ++i) a.w[i] = (i <= p->r) ? p->taps[i] : 0.f;
     dim3 grid((p->W + kTX - 1) / kTX, (out_rows + tile_rows - 1) / tile_rows, groups);
     p->last_tile_rows = tile_rows;
@@ -327,7 +361,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
     if (p->device >= 0) {
         if (p->last) cudaStreamSynchronize(p->last);
         cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
-        cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU);
+        cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
         cudaFree(p->dhost_in); cudaFree(p->dhost_out);
         for (auto &pair : p->ev)
             for (auto &e : pair)
@@ -372,7 +406,7 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     BF_CUDA(launch_diag_reset(p->ddiag, s));
     BF_CUDA(launch_normalize_groups(p->dpz, groups, p->kinfo.D, p->d, row1 - row0, p->W, p->mu, out,
                                     p->ddiag, 1.0f / p->M, (float)p->z_floor, s));
-    p->last_launches = 3;
+    p->last_launches = 4;
     p->last = s;
     return p->alias ? BF_W_ALIAS : BF_OK;
 }
@@ -418,7 +452,7 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k
     bf_status_t st = run_fused(p, f, p->H, 0, 0, p->H, k0, k1, s, &groups);
     if (st != BF_OK) return st;
     BF_CUDA(launch_finalize_partial(p->dpz, groups, p->kinfo.D, p->d, p->H, p->W, p->mu, rows_per_band, PZ, s));
-    p->last_launches = 2;
+    p->last_launches = 3;
     p->last = s;
     return BF_OK;
 }
