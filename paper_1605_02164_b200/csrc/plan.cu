@@ -155,27 +155,26 @@ void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows
     const int nx = (p->W + kTX - 1) / kTX;
     const int occ = std::max(1, ki.occupancy);
     const long long slots = (long long)sm_count() * occ;
-    // seconds per "row unit" (one 32-column row of one pass for all channels) per CTA
+    // seconds per "row unit" (one 32-column row of one FIR pass for all channels) per CTA,
+    // at ~60 % of the FP32 pipe shared by `occ` CTAs
     const double row_unit = 32.0 * 2.0 * (D + 1) * (2 * R + 1) / (128.0 / occ) / 1.9e9 / 0.6;
-    const double chunk_overhead_rows = 4.0;
     double best = 1e300;
     int bt = KB, bg = 1;
     const int rmax = (out_rows + KB - 1) / KB * KB;
     for (int ty = KB;; ty *= 2) {
         const int t = std::min(ty, rmax);
-        // keep the concurrently updated partial tiles L2-resident (~64 MB)
-        const double ws = (double)slots * 32.0 * t * (D + 1) * 4.0;
         const int ny = (out_rows + t - 1) / t;
         const int chunks = (std::min(t, out_rows) + KB - 1) / KB;
         for (int G = 1; G <= std::min(ns, 256); ++G) {
             const long long ctas = (long long)nx * ny * G;
-            if (ctas > 2147483647LL / 2) continue;
+            if (ctas > 2147483647LL / 2 || (long long)ny > 65535) continue;
             const int mg = (ns + G - 1) / G;
-            const double cta = mg * (2.0 * chunks * KB + 2.0 * R + chunks * chunk_overhead_rows) * row_unit;
+            // per sample: H rows (chunks*KB + 2R) and V rows (chunks*KB) run concurrently in
+            // the two warp groups; the 2R halo rows of the first chunk are not overlapped
+            const double cta = mg * (2.0 * chunks * KB + 4.0 * R + 2.0 * chunks) * row_unit + 2e-6;
             const long long waves = (ctas + slots - 1) / slots;
             double tt = waves * cta;
             if (G > 1) tt += (double)G * (D + 1) * out_rows * (double)p->W * 4.0 * 2.0 / 5e12;
-            if (ws > 64e6) tt *= 1.15;
             if (tt < best * 0.999) { best = tt; bt = t; bg = G; }
         }
         if (ty >= rmax) break;

@@ -17,6 +17,8 @@ ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--rows", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--samples", type=int, default=0)
+ap.add_argument("--tile-rows", type=int, default=0)
+ap.add_argument("--groups", type=int, default=0)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 rows = a.rows or cfg.H
@@ -25,6 +27,10 @@ s0, s1 = native.slab_bounds(cfg.H, y0, rows, cfg.radius)
 M = a.samples or cfg.M
 p = Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, M, cfg.seed, value_range=cfg.value_range)
 p.sample_freqs()
+if a.tile_rows:
+    p.set_option('tile_rows', a.tile_rows)
+if a.groups:
+    p.set_option('groups', a.groups)
 slab = torch.from_numpy(make_image_rows(cfg, s0, s1)).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for i in range(a.reps):
@@ -33,5 +39,5 @@ for i in range(a.reps):
     ev[1].record()
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1])
-    print(f"rep {i}: {ms:.3f} ms  {rows * cfg.W * M / ms / 1e6:.3e} px*samples/s  "
+    print(f"rep {i}: {ms:.3f} ms  {rows * cfg.W * M / ms * 1e3:.3e} px*samples/s  "
           f"tile_rows={p.info('tile_rows')} groups={p.info('groups')} ctas={p.info('ctas')}")
