@@ -161,6 +161,10 @@ void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows
     double best = 1e300;
     int bt = KB, bg = 1;
     const int rmax = (out_rows + KB - 1) / KB * KB;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+    cudaGetLastError();
+    const double pz_budget = std::min(0.25 * (double)(free_b + p->pz_bytes), 24.0 * 1073741824.0);
     for (int ty = KB;; ty *= 2) {
         const int t = std::min(ty, rmax);
         const int ny = (out_rows + t - 1) / t;
@@ -168,6 +172,10 @@ void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows
         for (int G = 1; G <= std::min(ns, 256); ++G) {
             const long long ctas = (long long)nx * ny * G;
             if (ctas > 2147483647LL / 2 || (long long)ny > 65535) continue;
+            // partial sums: G x (D+1) planes; keep them within a quarter of the free memory
+            // (at most 24 GiB), or 4 groups, whichever is larger
+            const double pz_bytes = (double)G * (D + 1) * out_rows * (double)p->W * 4.0;
+            if (G > 1 && pz_bytes > std::max(pz_budget, 4.0 * (D + 1) * out_rows * (double)p->W * 4.0)) continue;
             const int mg = (ns + G - 1) / G;
             // per sample: H rows (chunks*KB + 2R) and V rows (chunks*KB) run concurrently in
             // the two warp groups; the 2R halo rows of the first chunk are not overlapped
