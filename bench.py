@@ -154,6 +154,15 @@ def cpu_sample_size(cfg):
     return rows, samples
 
 
+def config_dict(cfg, world=1, mode="bands", **extra):
+    """The `config` object of the JSON line (same for both arms)."""
+    d = {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "d": cfg.d, "sigma_s": cfg.sigma_s,
+         "radius": cfg.radius, "N": cfg.N, "M": cfg.M, "seed": cfg.seed,
+         "parallelism": (f"{mode}{world}" if world > 1 else "single")}
+    d.update(extra)
+    return d
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -173,8 +182,7 @@ def run_reference(args, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "d": cfg.d, "sigma_s": cfg.sigma_s,
-                   "N": cfg.N, "M": cfg.M, "seed": cfg.seed},
+        "config": config_dict(cfg, args.gpus, args.mode),
         "cpu_baseline": {"value": value, "unit": "pixel*samples/s", "cores": info["threads"],
                          "kind": "oracle",
                          "sample": f"output rows {info['rows']} x {cfg.W} cols, first {samples} of "
@@ -191,7 +199,7 @@ def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
 
-    from paper_1605_02164_b200 import Plan
+    from paper_1605_02164_b200 import Plan, shard
     from workloads import make_image_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -206,28 +214,21 @@ def run_ours(args, cfg):
                 value_range=cfg.value_range)
     plan.sample_freqs()
 
-    # this rank's work
+    # this rank's work (DESIGN.md §8)
     if world == 1 or args.mode == "samples":
         y0, y1, s0, s1 = 0, cfg.H, 0, cfg.H
     else:
-        y0 = cfg.H * rank // world
-        y1 = cfg.H * (rank + 1) // world
-        s0, s1 = max(0, y0 - r), min(cfg.H, y1 + r)
+        y0, y1 = shard.band(cfg.H, world, rank)
+        s0, s1 = shard.slab_for_band(cfg.H, r, y0, y1)
     f_host = torch.from_numpy(make_image_rows(cfg, s0, s1))
     f = f_host.to(dev)
     rows = y1 - y0
     out = torch.empty((cfg.d, rows, cfg.W), dtype=torch.float32, device=dev)
-    k0 = cfg.M * rank // world if args.mode == "samples" else 0
-    k1 = cfg.M * (rank + 1) // world if args.mode == "samples" else cfg.M
-    PZ = None
+    k0, k1 = shard.sample_range(cfg.M, world, rank) if args.mode == "samples" else (0, cfg.M)
     if args.mode == "samples" and world > 1:
-        rpb = (cfg.H + world - 1) // world
-        PZ = torch.empty((cfg.d + 1) * cfg.H * cfg.W, dtype=torch.float32, device=dev)
-        band0 = rank * rpb
-        band1 = min(cfg.H, band0 + rpb)
-        PZ_band = torch.empty((cfg.d + 1) * (band1 - band0) * cfg.W, dtype=torch.float32, device=dev)
-        counts = [(cfg.d + 1) * (min(cfg.H, (g + 1) * rpb) - g * rpb) * cfg.W for g in range(world)]
-        out = torch.empty((cfg.d, band1 - band0, cfg.W), dtype=torch.float32, device=dev)
+        y0, y1 = shard.sample_band(cfg.H, world, rank)
+        rows = y1 - y0
+        out = torch.empty((cfg.d, rows, cfg.W), dtype=torch.float32, device=dev)
 
     stream = torch.cuda.current_stream()
     launches_per_step = 0
@@ -236,16 +237,13 @@ def run_ours(args, cfg):
         nonlocal launches_per_step
         if world == 1:
             plan.filter(f, out)
-            launches_per_step = 3
+            launches_per_step = 4           # pad, fused, diag reset, normalise
         elif args.mode == "bands":
-            plan.filter_rows(f, s0, y0, y1, out)
-            launches_per_step = 3
-        else:
-            plan.filter_partial(f, k0, k1, PZ, rows_per_band=rpb)
-            chunks = list(torch.split(PZ, counts))
-            dist.reduce_scatter(PZ_band, chunks)
-            plan.normalize(PZ_band, band0, band1, out)
+            shard.filter_bands(plan, f, s0, out=out)
             launches_per_step = 4
+        else:
+            shard.filter_samples(plan, f)   # partial (pad, fused, finalise), NCCL reduce-scatter, normalise
+            launches_per_step = 5
 
     flush = None
     in_bytes = f.numel() * 4
@@ -284,20 +282,37 @@ def run_ours(args, cfg):
     value = total_units / (ms_max / 1e3)
 
     # e2e through the C ABI with pinned host buffers (N = 1; bands: per-rank slabs)
+    # e2e through the public API with pinned HOST buffers, copies inside the timed region:
+    # N = 1: bf_vec_filter_host (H2D + filter + D2H in the C ABI); N > 1: each rank copies
+    # its input slab in, runs its step and copies its output band out; max over ranks.
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         fh = f_host.pin_memory()
-        oh = torch.empty((cfg.d, cfg.H, cfg.W), dtype=torch.float32).pin_memory()
-        plan.filter_host(fh, oh)
+        oh = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory()
+        n_e2e = max(1, min(args.steps, 3))
+
+        def e2e_step():
+            if world == 1:
+                plan.filter_host(fh, oh)
+            else:
+                f.copy_(fh, non_blocking=True)
+                step()
+                oh.copy_(out, non_blocking=True)
+                torch.cuda.synchronize()
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        n_e2e = max(1, min(args.steps, 3))
         for _ in range(n_e2e):
-            plan.filter_host(fh, oh)
-        e2e_s = time.perf_counter() - t0
-        e2e = {"value": cfg.H * cfg.W * cfg.M * n_e2e / e2e_s, "unit": "pixel*samples/s",
+            e2e_step()
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfg.H * cfg.W * cfg.M * n_e2e / float(e2e_s.item()), "unit": "pixel*samples/s",
                "h2d_bytes_per_step": fh.numel() * 4, "d2h_bytes_per_step": oh.numel() * 4,
-               "steps": n_e2e}
+               "steps": n_e2e, "per_rank_bytes": world > 1}
 
     clocks = clk.summary()
     pk = peaks()
@@ -328,10 +343,8 @@ def run_ours(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": cfg.name, "H": cfg.H, "W": cfg.W, "d": cfg.d, "sigma_s": cfg.sigma_s,
-                       "radius": r, "N": cfg.N, "M": cfg.M, "seed": cfg.seed,
-                       "parallelism": (f"{args.mode}{world}" if world > 1 else "single"),
-                       "l2": l2_note, "tile_rows": plan.info("tile_rows"), "groups": plan.info("groups")},
+            "config": config_dict(cfg, world, args.mode, l2=l2_note, tile_rows=plan.info("tile_rows"),
+                                  groups=plan.info("groups")),
             "mpix_per_s": cfg.H * cfg.W * args.steps / (ms_max / 1e3) / 1e6,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,

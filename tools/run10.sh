@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke exit $?"
+timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench_r01_b.json 2> gpurun_out/bench_r01_b.err
+echo "bench exit $?"
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_torchrun1.json 2> gpurun_out/bench_torchrun1.err
+echo "torchrun exit $?"
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+echo "ref exit $?"
