@@ -164,6 +164,8 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *   "value_range" nominal data range R used for the alias warning (default 255)
  *   "tile_rows"   force the row-tile height of the fused kernel (0 = auto)
  *   "groups"      force the number of sample groups (0 = auto)
+ *   "variant"     fused-kernel variant: 0 auto, 1 shared-memory ring, 2 tensor-memory
+ *                 ring (d <= 3 only); BF_E_UNSUPPORTED if not compiled for the plan
  *   "profile"     1: record CUDA events around every fused-kernel launch on the
  *                 launching stream (read back with bf_vec_plan_info
  *                 "fused_ns_total" / "fused_calls"); 0: off. Setting it resets the totals.
@@ -175,7 +177,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value
  * bf_vec_plan_info -- integers describing the plan (for tooling and tests):
  *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
  *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
- *   "regs", "occupancy", "alias", and (option "profile") "fused_ns_total",
+ *   "regs", "occupancy", "alias", "variant", and (option "profile") "fused_ns_total",
  *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
  *   an unknown name.
  */

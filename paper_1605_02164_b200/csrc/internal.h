@@ -46,10 +46,11 @@ struct KernelInfo {
     size_t smem;
     int regs;
     int occupancy;        // CTAs per SM (from the occupancy API)
+    int variant;          // 1: shared-memory ring (v3), 2: tensor-memory ring (v4)
 };
 
 // Kernel-set dispatch (mcsf_fused.cu). Returns false if no instance fits.
-bool fused_select(int d, int r, KernelInfo *info);
+bool fused_select(int d, int r, int variant, KernelInfo *info);
 cudaError_t fused_launch(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s);
 
 // Reflect-padded, centred, interleaved copy of the input for the TMA loads (pad.cu)
@@ -93,6 +94,7 @@ struct bf_vec_plan_s {
     double value_range = 255.0;
     int force_tile_rows = 0;
     int force_groups = 0;
+    int force_variant = 0;     // 0 auto, 1 v3 (smem ring), 2 v4 (TMEM ring)
     // device state (lazily created)
     int device = -1;
     bool sampled = false;

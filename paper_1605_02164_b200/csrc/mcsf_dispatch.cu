@@ -7,14 +7,14 @@ namespace bfvec {
 
 #define BFV_DS(X) X(1) X(2) X(3) X(4) X(8)
 #define BFV_DECL(D)                                                 \
-    bool fused_select_d##D(int r, KernelInfo *info);                \
+    bool fused_select_d##D(int r, int variant, KernelInfo *info);                \
     cudaError_t fused_launch_d##D(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s);
 BFV_DS(BFV_DECL)
 #undef BFV_DECL
 
-bool fused_select(int d, int r, KernelInfo *info) {
+bool fused_select(int d, int r, int variant, KernelInfo *info) {
 #define BFV_TRY(D) \
-    if (d <= D) return fused_select_d##D(r, info);
+    if (d <= D) return fused_select_d##D(r, variant, info);
     BFV_DS(BFV_TRY)
 #undef BFV_TRY
     return false;

@@ -36,24 +36,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <utility>
-
-#include "internal.h"
+#include "kernel_common.cuh"
 
 namespace bfvec {
 namespace {
-
-constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
-// stride (in float2) of a `modcs` row: >= n, == 2 (mod 4) so the H-pass LDS.128
-// of 8 consecutive rows hit 8 distinct 4-bank groups.
-constexpr int cs_stride(int n) {
-    int s = round_up(n, 2);
-    while (s % 4 != 2) s += 2;
-    return s;
-}
-// stride (in floats) of a `modf` row: >= n, == 2 (mod 4): LDS.64 of 16 consecutive rows
-// hit 16 distinct 2-bank groups (an odd multiple of 2 is a bijection mod 32).
-constexpr int f_stride(int n) { return cs_stride(n); }
 
 template <int D_, int R_, int NA_, int KB_, int SH_>
 struct Cfg {
@@ -99,73 +85,21 @@ struct Cfg {
 };
 
 // ---------------------------------------------------------------------------
-// PTX helpers: mbarrier + TMA
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t saddr(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t done;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(saddr(bar)), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
-                                            int c2, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(saddr(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(saddr(bar))
-        : "memory");
-}
-
-template <class F, int... Js>
-__device__ __forceinline__ void static_for_impl(F &&f, std::integer_sequence<int, Js...>) {
-    (f(std::integral_constant<int, Js>{}), ...);
-}
-// compile-time loop: f(std::integral_constant<int, j>) for j = 0..N-1, always fully
-// expanded (NVVM's unroller gives up on the larger FIR bodies, which would turn the
-// taps into runtime constant loads)
-template <int N, class F>
-__device__ __forceinline__ void static_for(F &&f) {
-    static_for_impl(f, std::make_integer_sequence<int, N>{});
-}
-
-__device__ __forceinline__ float2 ffma2(float w, float2 v, float2 acc) {
-    return __ffma2_rn(make_float2(w, w), v, acc);
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void named_sync(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(N) : "memory");
-}
-
-// ---------------------------------------------------------------------------
 // producer stages
 // ---------------------------------------------------------------------------
 // modulate n rows of fbuf; row `row` is emitted row g0 + row
 template <class C>
 __device__ __forceinline__ void modulate(int ta, const float *fbuf, float2 *modcs, float *modf, float2 *csring,
                                          const float (&tk)[C::D], int g0, int n) {
-    for (int it = ta; it < C::SH * C::WIN; it += C::NA) {
+    // fixed trip count, fully unrolled: the per-pixel LDS -> FFMA -> MUFU -> STS chains of
+    // all of a thread's pixels interleave instead of running back to back
+    constexpr int PER = (C::SH * C::WIN + C::NA - 1) / C::NA;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int it = ta + i * C::NA;
         const int row = it / C::WIN;
         const int j = it - row * C::WIN;
-        if (row >= n) continue;
+        if (it >= C::SH * C::WIN || row >= n) continue;
         const float *px = fbuf + (row * C::WIN + j) * C::DP;
         float fv[C::D];
 #pragma unroll

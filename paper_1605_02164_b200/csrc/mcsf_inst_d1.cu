@@ -1,28 +1,54 @@
 // mcsf_inst_d1.cu -- fused-kernel instances for D = 1 (one translation unit per D so
-// the large fully-expanded FIR bodies compile in parallel). Cfg<D, R, NA, KB, SH> (NA = producer threads).
+// the large fully-expanded FIR bodies compile in parallel).
+//   v3 (shared-memory ring, mcsf_fused.cuh): Cfg<D, R, NA, KB, SH> (NA = producer threads)
+//   v4 (tensor-memory ring, mcsf_tmem.cuh):  CfgT<D, R, 16>
 #include "mcsf_fused.cuh"
+#include "mcsf_tmem.cuh"
 
 namespace bfvec {
 
 #define BFV_INSTANCES(X) X(1, 2, 64, 16, 16) X(1, 6, 64, 16, 16) X(1, 15, 64, 16, 16) X(1, 32, 64, 16, 16) X(1, 64, 64, 16, 16)
+#define BFV_TMEM_INSTANCES(X) X(1, 6) X(1, 15) X(1, 24) X(1, 32) X(1, 48)
 
-bool fused_select_d1(int r, KernelInfo *info) {
-    int best = 1 << 30;
-#define BFV_PICK(D_, R_, NT_, KB_, SH_) \
+// variant: 0 auto (v4 where compiled), 1 force v3, 2 force v4
+bool fused_select_d1(int r, int variant, KernelInfo *info) {
+    int best = 1 << 30, bestT = 1 << 30;
+#define BFV_PICK(D_, R_, NA_, KB_, SH_) \
     if (R_ >= r && R_ < best) best = R_;
     BFV_INSTANCES(BFV_PICK)
 #undef BFV_PICK
+#define BFV_PICKT(D_, R_) \
+    if (R_ >= r && R_ < bestT) bestT = R_;
+    BFV_TMEM_INSTANCES(BFV_PICKT)
+#undef BFV_PICKT
+    const bool use_t = bestT != (1 << 30) && variant != 1 && (variant == 2 || bestT <= best);
+    if (use_t) {
+#define BFV_FILLT(D_, R_) \
+    if (R_ == bestT) fill_info_tmem<CfgT<D_, R_, 16>>(info);
+        BFV_TMEM_INSTANCES(BFV_FILLT)
+#undef BFV_FILLT
+        info->variant = 2;
+        return true;
+    }
     if (best == (1 << 30)) return false;
-#define BFV_FILL(D_, R_, NT_, KB_, SH_) \
-    if (R_ == best) fill_info<Cfg<D_, R_, NT_, KB_, SH_>>(info);
+#define BFV_FILL(D_, R_, NA_, KB_, SH_) \
+    if (R_ == best) fill_info<Cfg<D_, R_, NA_, KB_, SH_>>(info);
     BFV_INSTANCES(BFV_FILL)
 #undef BFV_FILL
+    info->variant = 1;
     return true;
 }
 
 cudaError_t fused_launch_d1(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s) {
-#define BFV_LAUNCH(D_, R_, NT_, KB_, SH_) \
-    if (info.R == R_) return launch_cfg<Cfg<D_, R_, NT_, KB_, SH_>>(a, grid, s);
+    if (info.variant == 2) {
+#define BFV_LAUNCHT(D_, R_) \
+    if (info.R == R_) return launch_tmem<CfgT<D_, R_, 16>>(a, grid, s);
+        BFV_TMEM_INSTANCES(BFV_LAUNCHT)
+#undef BFV_LAUNCHT
+        return cudaErrorInvalidValue;
+    }
+#define BFV_LAUNCH(D_, R_, NA_, KB_, SH_) \
+    if (info.R == R_) return launch_cfg<Cfg<D_, R_, NA_, KB_, SH_>>(a, grid, s);
     BFV_INSTANCES(BFV_LAUNCH)
 #undef BFV_LAUNCH
     return cudaErrorInvalidValue;

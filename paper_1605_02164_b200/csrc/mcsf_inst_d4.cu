@@ -6,7 +6,8 @@ namespace bfvec {
 
 #define BFV_INSTANCES(X) X(4, 6, 160, 16, 8) X(4, 15, 160, 16, 8) X(4, 32, 160, 16, 8) X(4, 48, 160, 16, 8)
 
-bool fused_select_d4(int r, KernelInfo *info) {
+bool fused_select_d4(int r, int variant, KernelInfo *info) {
+    (void)variant;   // v3 only for D = 4
     int best = 1 << 30;
 #define BFV_PICK(D_, R_, NT_, KB_, SH_) \
     if (R_ >= r && R_ < best) best = R_;
@@ -17,6 +18,7 @@ bool fused_select_d4(int r, KernelInfo *info) {
     if (R_ == best) fill_info<Cfg<D_, R_, NT_, KB_, SH_>>(info);
     BFV_INSTANCES(BFV_FILL)
 #undef BFV_FILL
+    info->variant = 1;
     return true;
 }
 

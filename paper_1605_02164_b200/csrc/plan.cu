@@ -129,7 +129,7 @@ bf_status_t ensure_device(bf_vec_plan_t p) {
     BF_CUDA(cudaMalloc(&p->dQ, sizeof(double) * 64));
     BF_CUDA(cudaMalloc(&p->dgamma, sizeof(double) * 8));
     BF_CUDA(cudaMalloc(&p->ddiag, 16));
-    if (!fused_select(p->d, p->r, &p->kinfo)) return BF_E_UNSUPPORTED;
+    if (!fused_select(p->d, p->r, p->force_variant, &p->kinfo)) return BF_E_UNSUPPORTED;
     p->kinfo_ok = true;
     p->device = dev;
     return BF_OK;
@@ -554,6 +554,16 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
     }
     if (!std::strcmp(name, "tile_rows")) { if (v < 0) return BF_E_ARG; p->force_tile_rows = (int)v; return BF_OK; }
     if (!std::strcmp(name, "groups")) { if (v < 0) return BF_E_ARG; p->force_groups = (int)v; return BF_OK; }
+    if (!std::strcmp(name, "variant")) {
+        if (v < 0 || v > 2) return BF_E_ARG;
+        p->force_variant = (int)v;
+        if (p->device >= 0) {   // re-select the kernel instance
+            bfvec::KernelInfo ki;
+            if (!fused_select(p->d, p->r, p->force_variant, &ki)) return BF_E_UNSUPPORTED;
+            p->kinfo = ki;
+        }
+        return BF_OK;
+    }
     if (!std::strcmp(name, "profile")) {
         collect_profile(p);
         p->profile = v != 0.0;
@@ -577,7 +587,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"tile_rows", p->last_tile_rows}, {"groups", p->last_groups}, {"ctas", p->last_ctas},
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
-        {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0},
+        {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
     };
     for (auto &e : tab)
         if (!std::strcmp(e.n, name)) { *value = e.v; return BF_OK; }
