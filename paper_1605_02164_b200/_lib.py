@@ -2,7 +2,7 @@
 
 Argument marshalling only. There is no CPU fallback: if the in-tree library
 is missing, importing the binding raises (build it with
-``python -m paper_1605_02164_b200.build``).
+``python paper_1605_02164_b200/build.py``).
 """
 import ctypes
 import os
@@ -45,7 +45,7 @@ def load():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"libbfvec.so not built ({LIB_PATH}); run "
-                              "`python -m paper_1605_02164_b200.build`")
+                              "`python paper_1605_02164_b200/build.py`")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (args, res) in SIGNATURES.items():
             fn = getattr(lib, name)

@@ -1,6 +1,6 @@
 """Build libbfvec.so (the C-ABI library) in-tree for sm_100a.
 
-    python -m paper_1605_02164_b200.build [--force]
+    python paper_1605_02164_b200/build.py [--force]
 
 Each .cu under csrc/ is compiled by nvcc in parallel, then linked into
 paper_1605_02164_b200/libbfvec.so (static CUDA runtime). ptxas resource usage
