@@ -58,7 +58,10 @@ typedef enum {
  * bf_vec_plan -- Algorithm 1 setup, L210-214.
  *   H, W      image height and width, >= 1
  *   d         vector dimension, 1 <= d <= 8
- *   sigma_s   spatial std-dev (pixels) > 0; window radius r = ceil(3 sigma_s) <= 64
+ *   sigma_s   spatial std-dev (pixels) > 0; window radius r = ceil(3 sigma_s). The
+ *             truncated-window (FIR) engine and bf_vec_direct need r <= 64 (else they return
+ *             BF_E_UNSUPPORTED); the recursive engine (option "engine" = 1) accepts any
+ *             r <= 2^20
  *   C         host, d x d row-major symmetric positive-definite covariance (Eq. (1))
  *   N         raised-cosine order, even, 2 <= N <= 64 (Eq. (9))
  *   M         number of Monte Carlo samples (the paper's T), M >= 1
@@ -165,7 +168,24 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *   "tile_rows"   force the row-tile height of the fused kernel (0 = auto)
  *   "groups"      force the number of sample groups (0 = auto)
  *   "variant"     fused-kernel variant: 0 auto, 1 shared-memory ring, 2 tensor-memory
- *                 ring (d <= 3 only); BF_E_UNSUPPORTED if not compiled for the plan
+ *                 ring (d <= 3 only), 3 tensor-memory ring with two consumer warps per
+ *                 (cos, sin) pair (d <= 3, r in (30, 48]); BF_E_UNSUPPORTED if not compiled
+ *                 for the plan
+ *   "engine"      how Alg. 1 step 10 convolves: 0 (default) the truncated
+ *                 separable window [-r, r] of Eq. (1) / "spatial_kernel", O(r) per pixel-sample
+ *                 (fused sm_100a kernel); 1 the recursive O(1)-in-sigma_s engine of PAPER.md:204
+ *                 (Deriche 1993): spatial kernel g(m) = h(|m|) / sum h of Deriche's 4th-order
+ *                 recursive Gaussian over the reflected-periodic image (reading R16,
+ *                 §11). Engine 1 filters whole images only (bf_vec_filter, _host, _partial;
+ *                 bf_vec_filter_rows returns BF_E_UNSUPPORTED for a proper band) and ignores
+ *                 "spatial_kernel", "variant", "tile_rows" and "groups".
+ *   "rec_batch"   engine 1: samples per batch (0 = auto from free device memory; each sample
+ *                 in flight holds 5 (d+1) fp32 planes of H x W scratch)
+ *   "spatial_kernel" separable spatial taps on the window [-r, r], r = ceil(3 sigma_s):
+ *                 0 Gaussian of Eq. (1) (default), 1 box w(m) = 1, 2 hat w(m) = r + 1 - |m|
+ *                 ("any arbitrary spatial filter (such as a box or hat filter)";
+ *                 DESIGN.md reading R15); taps are normalised to sum 1. Applies to the MC
+ *                 filter and to bf_vec_direct.
  *   "profile"     1: record CUDA events around every fused-kernel launch on the
  *                 launching stream (read back with bf_vec_plan_info
  *                 "fused_ns_total" / "fused_calls"); 0: off. Setting it resets the totals.
@@ -177,7 +197,8 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value
  * bf_vec_plan_info -- integers describing the plan (for tooling and tests):
  *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
  *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
- *   "regs", "occupancy", "alias", "variant", and (option "profile") "fused_ns_total",
+ *   "regs", "occupancy", "alias", "variant", "spatial_kernel", "engine", "rec_batch" (last batch
+ *   size), "fir_supported" (r <= 64), and (option "profile") "fused_ns_total",
  *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
  *   an unknown name.
  */

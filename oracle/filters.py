@@ -38,12 +38,12 @@ def _rotate(f, Q):
     return np.einsum("ck,chw->khw", np.asarray(Q, dtype=np.float64), f.astype(np.float64))
 
 
-def mc_filter_bruteforce(f, Q, alpha, N, Y, sigma_s):
+def mc_filter_bruteforce(f, Q, alpha, N, Y, sigma_s, spatial="gaussian"):
     """O1 over the whole image. Returns (S, P, Z): S (d,H,W), P (d,H,W), Z (H,W)."""
     f64 = np.asarray(f, dtype=np.float64)
     d, H, W = f64.shape
-    r = _plan.radius(sigma_s)
-    w = _plan.spatial_taps(sigma_s)
+    w = _plan.spatial_window(sigma_s, spatial)
+    r = (len(w) - 1) // 2
     g = _rotate(f64, Q)
     Yg = np.asarray(Y, dtype=np.float64) * _plan.gammas(alpha, N)[None, :]   # (T, d)
     P = np.zeros((d, H, W))
@@ -60,13 +60,13 @@ def mc_filter_bruteforce(f, Q, alpha, N, Y, sigma_s):
     return P / Z[None], P, Z
 
 
-def mc_filter_pixels(get_rows, H, W, pixels, Q, alpha, N, Y, sigma_s):
+def mc_filter_pixels(get_rows, H, W, pixels, Q, alpha, N, Y, sigma_s, spatial="gaussian"):
     """O1 at selected pixels of an image of any size.
 
     get_rows(y0, y1) must return planar rows [y0, y1) of the full image.
     pixels: iterable of (y, x). Returns (S (n,d), P (n,d), Z (n,))."""
-    r = _plan.radius(sigma_s)
-    w = _plan.spatial_taps(sigma_s)
+    w = _plan.spatial_window(sigma_s, spatial)
+    r = (len(w) - 1) // 2
     om = np.outer(w, w)                                                       # (2r+1, 2r+1)
     Yg = np.asarray(Y, dtype=np.float64) * _plan.gammas(alpha, N)[None, :]
     Q = np.asarray(Q, dtype=np.float64)
@@ -93,13 +93,13 @@ def mc_filter_pixels(get_rows, H, W, pixels, Q, alpha, N, Y, sigma_s):
     return np.array(out_S), np.array(out_P), np.array(out_Z)
 
 
-def kernel_filter_bruteforce(f, Q, sigma_s, psi_fn):
+def kernel_filter_bruteforce(f, Q, sigma_s, psi_fn, spatial="gaussian"):
     """Eq. (5)-(6) with range kernel psi_fn(dg) where dg has shape (H, W, d).
     psi_fn may return complex values; real parts are taken (reading R4)."""
     f64 = np.asarray(f, dtype=np.float64)
     d, H, W = f64.shape
-    r = _plan.radius(sigma_s)
-    w = _plan.spatial_taps(sigma_s)
+    w = _plan.spatial_window(sigma_s, spatial)
+    r = (len(w) - 1) // 2
     g = _rotate(f64, Q)
     P = np.zeros((d, H, W))
     Z = np.zeros((H, W))
@@ -113,12 +113,12 @@ def kernel_filter_bruteforce(f, Q, sigma_s, psi_fn):
     return P / Z[None], P, Z
 
 
-def direct_bruteforce(f, C, sigma_s):
+def direct_bruteforce(f, C, sigma_s, spatial="gaussian"):
     """Eq. (2)-(3): phi(x) = exp(-x^T C^-1 x / 2) on x = f(i-j) - f(i)."""
     f64 = np.asarray(f, dtype=np.float64)
     d, H, W = f64.shape
-    r = _plan.radius(sigma_s)
-    w = _plan.spatial_taps(sigma_s)
+    w = _plan.spatial_window(sigma_s, spatial)
+    r = (len(w) - 1) // 2
     Cinv = np.linalg.inv(np.asarray(C, dtype=np.float64))
     num = np.zeros((d, H, W))
     den = np.zeros((H, W))

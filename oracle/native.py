@@ -50,11 +50,12 @@ def set_threads(n: int):
     lib.omp_set_num_threads(int(n))
 
 
-def mcsf_alg1(f_slab, H, slab_row0, out_row0, out_rows, Q, alpha, N, Y, sigma_s, imag=False):
+def mcsf_alg1(f_slab, H, slab_row0, out_row0, out_rows, Q, alpha, N, Y, sigma_s, imag=False,
+              spatial="gaussian"):
     """Algorithm 1 on a row slab. f_slab: planar (d, slab_rows, W) float32 holding
     rows [slab_row0, slab_row0 + slab_rows) of an image of height H.
     Returns (S, P, Z[, Pim, Zim]) for output rows [out_row0, out_row0 + out_rows):
-    S = Re P / Re Z (reading R4)."""
+    S = Re P / Re Z (reading R4). ``spatial`` selects the taps (plan.spatial_window)."""
     lib = _load()
     f_slab = np.ascontiguousarray(f_slab, dtype=np.float32)
     d, slab_rows, W = f_slab.shape
@@ -62,8 +63,8 @@ def mcsf_alg1(f_slab, H, slab_row0, out_row0, out_rows, Q, alpha, N, Y, sigma_s,
     alpha = np.ascontiguousarray(alpha, dtype=np.float64)
     Y = np.ascontiguousarray(Y, dtype=np.int32)
     T = Y.shape[0]
-    w = np.ascontiguousarray(_plan.spatial_taps(sigma_s))
-    r = _plan.radius(sigma_s)
+    w = np.ascontiguousarray(_plan.spatial_window(sigma_s, spatial))
+    r = (len(w) - 1) // 2
     P = np.empty((d, out_rows, W))
     Z = np.empty((out_rows, W))
     Pim = np.empty((d, out_rows, W)) if imag else None
@@ -77,19 +78,19 @@ def mcsf_alg1(f_slab, H, slab_row0, out_row0, out_rows, Q, alpha, N, Y, sigma_s,
     return (S, P, Z, Pim, Zim) if imag else (S, P, Z)
 
 
-def mcsf_full(f, Q, alpha, N, Y, sigma_s, imag=False):
+def mcsf_full(f, Q, alpha, N, Y, sigma_s, imag=False, spatial="gaussian"):
     d, H, W = f.shape
-    return mcsf_alg1(f, H, 0, 0, H, Q, alpha, N, Y, sigma_s, imag=imag)
+    return mcsf_alg1(f, H, 0, 0, H, Q, alpha, N, Y, sigma_s, imag=imag, spatial=spatial)
 
 
-def direct(f_slab, H, slab_row0, out_row0, out_rows, C, sigma_s):
+def direct(f_slab, H, slab_row0, out_row0, out_rows, C, sigma_s, spatial="gaussian"):
     """Exact filter Eq. (2)-(3) on a row slab; returns (d, out_rows, W)."""
     lib = _load()
     f_slab = np.ascontiguousarray(f_slab, dtype=np.float32)
     d, slab_rows, W = f_slab.shape
     Cinv = np.ascontiguousarray(np.linalg.inv(np.asarray(C, dtype=np.float64)))
-    w = np.ascontiguousarray(_plan.spatial_taps(sigma_s))
-    r = _plan.radius(sigma_s)
+    w = np.ascontiguousarray(_plan.spatial_window(sigma_s, spatial))
+    r = (len(w) - 1) // 2
     out = np.empty((d, out_rows, W))
     rc = lib.oracle_direct(H, W, d, _ptr(f_slab), slab_row0, slab_rows, out_row0, out_rows,
                            _ptr(Cinv), r, _ptr(w), _ptr(out))
@@ -98,9 +99,9 @@ def direct(f_slab, H, slab_row0, out_row0, out_rows, C, sigma_s):
     return out
 
 
-def direct_full(f, C, sigma_s):
+def direct_full(f, C, sigma_s, spatial="gaussian"):
     d, H, W = f.shape
-    return direct(f, H, 0, 0, H, C, sigma_s)
+    return direct(f, H, 0, 0, H, C, sigma_s, spatial=spatial)
 
 
 def slab_bounds(H, out_row0, out_rows, r):

@@ -11,7 +11,8 @@
 namespace bfvec {
 
 constexpr int kMaxD = 8;
-constexpr int kMaxR = 64;
+constexpr int kMaxR = 64;          // largest FIR radius (truncated-window engine)
+constexpr int kMaxRec = 1 << 20;   // largest r = ceil(3 sigma_s) the plan accepts (recursive engine)
 constexpr int kTX = 32;            // output columns per strip (one warp of lanes)
 
 // Arguments of the fused MCSF kernel (one launch = one output band, one sample range).
@@ -73,6 +74,31 @@ cudaError_t launch_normalize_raw(const float *PZ, int d, int rows, int W, float 
                                  float inv_m, float z_floor, cudaStream_t s);
 cudaError_t launch_diag_reset(float *diag, cudaStream_t s);
 
+// Recursive engine (recursive.cu; option "engine" = 1, reading R16).
+// One axis of the separable recursive Gaussian: two complex poles z_j, residues A_j (normalised
+// so the kernel sums to 1), g0 = g(0), z_j^n and 1 / (1 - z_j^2n) for the reflected-periodic
+// initial state of a line of length n, and the number of head / tail terms summed for it.
+struct RecAxis {
+    float zr[2], zi[2];
+    float ar[2], ai[2];
+    float g0;
+    float znr[2], zni[2];
+    float invr[2], invi[2];
+    int lh;
+};
+struct RecArgs {
+    const float *f;       // (d, H, W) input
+    const float *t;       // (M, d) frequency table
+    float *y1, *y2;       // (nb, 2(d+1), H, W) scratch: row-pass output, column forward partial
+    float *pz;            // (nb, d+1, H, W): planes 0..d-1 = P' (centred), d = Z; group b <- sample k0 + b
+    float mu[kMaxD];      // centring (reading R12)
+    int d, H, W;
+    int k0, nb;           // samples [k0, k0 + nb) of this batch
+    int first;            // 1: store into pz, 0: accumulate
+    RecAxis row, col;
+};
+cudaError_t launch_recursive(const RecArgs &a, cudaStream_t s);
+
 // Direct filter (direct.cu)
 cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const float *w,
                           const float *A /* d x d: diag(alpha) Q^T scaled */, float *U,
@@ -95,6 +121,12 @@ struct bf_vec_plan_s {
     int force_tile_rows = 0;
     int force_groups = 0;
     int force_variant = 0;     // 0 auto, 1 v3 (smem ring), 2 v4 (TMEM ring)
+    int spatial = 0;           // spatial taps: 0 Gaussian (Eq. (1)), 1 box, 2 hat (reading R15)
+    int engine = 0;            // 0 truncated FIR (Eq. (1) window), 1 recursive Deriche (reading R16)
+    int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
+    float *drec = nullptr;     // recursive engine scratch (y1, y2)
+    size_t drec_bytes = 0;
+    int last_batch = 0;
     // device state (lazily created)
     int device = -1;
     bool sampled = false;

@@ -23,7 +23,7 @@
 namespace bfvec {
 namespace {
 
-template <int D_, int R_, int KB_>
+template <int D_, int R_, int KB_, int CW_ = 1>
 struct CfgT {
     static constexpr int D = D_;
     static constexpr int R = R_;
@@ -32,7 +32,9 @@ struct CfgT {
     static constexpr int TX = kTX;
     static constexpr int NP = D + 1;         // (cos, sin) pairs: Z, P_0..P_{D-1}; one TMEM quarter each
     static constexpr int NA = 256;           // producer threads: warp w -> pair w % 4, rows 8*(w / 4) .. +8
-    static constexpr int NB = 128;           // consumer threads: warp 8 + p -> pair p (quarter p)
+    static constexpr int CW = CW_;           // consumer warps per pair: warp 8 + w -> pair w & 3,
+    static constexpr int OR = KB / CW_;      //   output rows OR (w >> 2) .. +OR of every chunk
+    static constexpr int NB = 128 * CW_;     // consumer threads
     static constexpr int NT = NA + NB;
     static constexpr int DP = 4;
     static constexpr int WIN = TX + 2 * R;
@@ -57,6 +59,7 @@ struct CfgT {
     static constexpr int MINB = 1;
     static_assert(D >= 1 && D <= 3, "one TMEM lane quarter per pair");
     static_assert(KB == 16, "one aligned 16-row block per chunk");
+    static_assert(CW_ == 1 || CW_ == 2, "one or two consumer warps per pair");
     static_assert(2 * HROWS <= 512, "TMEM columns");
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(WIN <= 256, "TMA box dimension");
@@ -69,6 +72,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float2 (&v)[8]) 
         "f"(v[0].x), "f"(v[0].y), "f"(v[1].x), "f"(v[1].y), "f"(v[2].x), "f"(v[2].y), "f"(v[3].x), "f"(v[3].y),
         "f"(v[4].x), "f"(v[4].y), "f"(v[5].x), "f"(v[5].y), "f"(v[6].x), "f"(v[6].y), "f"(v[7].x), "f"(v[7].y)
         : "memory");
+}
+
+// wait for every outstanding tcgen05.ld of this thread, then tie the destination registers
+// to the wait so no use of them can be scheduled above it
+__device__ __forceinline__ void tmem_wait_ld(float2 (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) asm volatile("" : "+f"(v[i].x), "+f"(v[i].y));
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float2 (&v)[16]) {
@@ -247,7 +258,10 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem_kernel(const __grid_consta
             }
         } else {
             // ============================ CONSUMERS ===========================
-            const int p = warp & 3;                         // pair == TMEM quarter (warps 8..11)
+            // warp 8 + w: pair p = w & 3 (TMEM quarter p = warp % 4); part h = w >> 2 owns
+            // output rows OR h .. OR h + OR - 1 of every chunk
+            const int p = warp & 3;
+            const int h = (warp - C::NA / 32) >> 2;
             const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16);
             const int x = x0 + lane;
             const bool active = p < C::NP;
@@ -255,59 +269,81 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem_kernel(const __grid_consta
             const long long plane_out = (long long)a.out_rows * a.W;
             const int plane = (p == 0) ? C::D : p - 1;
             float *pzp = a.pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
-            int q = 0;
-            for (int k = gk0; k < gk1; ++k) {
-                const bool first_k = (k == gk0);
-                const int gs = (k - gk0) * rows_per_sample;
-                for (int ci = 0; ci < nchunks; ++ci, ++q) {
-                    const int cy = ty0 + ci * C::KB;
-                    float *dst = pzp + (long long)(cy - a.out_row0) * a.W;
-                    float old[C::KB];
+            auto body = [&](auto HH) {
+                constexpr int OR = C::OR;
+                constexpr int H0 = OR * decltype(HH)::value;       // first output row of this part
+                constexpr int JB0 = H0 / 16;                       // first 16-row TMEM block read
+                constexpr int JB1 = (H0 + OR - 1 + 2 * C::R) / 16 + 1;  // one past the last block read
+                int q = 0;
+                for (int k = gk0; k < gk1; ++k) {
+                    const bool first_k = (k == gk0);
+                    const int gs = (k - gk0) * rows_per_sample;
+                    for (int ci = 0; ci < nchunks; ++ci, ++q) {
+                        const int cy = ty0 + ci * C::KB + H0;
+                        float *dst = pzp + (long long)(cy - a.out_row0) * a.W;
+                        // prefetch the old partial sums before waiting (their L2 latency overlaps
+                        // the wait and the FIR; 16 registers, no spill at <= 168)
+                        float old[OR];
 #pragma unroll
-                    for (int o = 0; o < C::KB; ++o) {
-                        const bool ok = active && xok && (cy + o < ty1);
-                        old[o] = (!first_k && ok) ? dst[(long long)o * a.W] : 0.f;
-                    }
-                    mbar_wait(&full[q & 1], (q >> 1) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    float2 acc[C::KB];
+                        for (int o = 0; o < OR; ++o) {
+                            const bool ok = active && xok && (cy + o < ty1);
+                            old[o] = (!first_k && ok) ? dst[(long long)o * a.W] : 0.f;
+                        }
+                        mbar_wait(&full[q & 1], (q >> 1) & 1);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        float2 acc[OR];
 #pragma unroll
-                    for (int o = 0; o < C::KB; ++o) acc[o] = make_float2(0.f, 0.f);
-                    const int b0 = (gs + ci * C::KB) % C::HROWS;   // multiple of 16
-                    // window rows j in [0, A) (taps only for j < KB + 2R), 16 per TMEM load
-                    static_for<C::A / 16>([&](auto B) {
-                        constexpr int bj = decltype(B)::value;
-                        int slot = b0 + 16 * bj;
-                        if (slot >= C::HROWS) slot -= C::HROWS;
-                        float2 v[16];
-                        tmem_ld32(tq + 2 * slot, v);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        static_for<16>([&](auto JJ) {
-                            constexpr int j = 16 * bj + decltype(JJ)::value;
-                            static_for<C::KB>([&](auto O) {
-                                constexpr int o = decltype(O)::value;
-                                constexpr int m = j - o - C::R;
-                                if constexpr (m >= -C::R && m <= C::R)
-                                    acc[o] = ffma2(a.w[m < 0 ? -m : m], v[decltype(JJ)::value], acc[o]);
+                        for (int o = 0; o < OR; ++o) acc[o] = make_float2(0.f, 0.f);
+                        const int b0 = (gs + ci * C::KB) % C::HROWS;   // multiple of 16
+                        float2 v[2][16];
+                        auto slot_of = [&](int bj) {
+                            const int slot = b0 + 16 * bj;
+                            return slot >= C::HROWS ? slot - C::HROWS : slot;
+                        };
+                        tmem_ld32(tq + 2 * slot_of(JB0), v[JB0 & 1]);
+                        tmem_wait_ld(v[JB0 & 1]);
+                        // block bj is in registers; the load of block bj + 1 overlaps its FFMA2s
+                        static_for<JB1 - JB0>([&](auto B) {
+                            constexpr int bj = JB0 + decltype(B)::value;
+                            if constexpr (bj + 1 < JB1) tmem_ld32(tq + 2 * slot_of(bj + 1), v[(bj + 1) & 1]);
+                            static_for<16>([&](auto JJ) {
+                                constexpr int j = 16 * bj + decltype(JJ)::value;
+                                static_for<OR>([&](auto O) {
+                                    constexpr int o = H0 + decltype(O)::value;
+                                    constexpr int m = j - o - C::R;
+                                    if constexpr (m >= -C::R && m <= C::R)
+                                        acc[o - H0] = ffma2(a.w[m < 0 ? -m : m], v[bj & 1][decltype(JJ)::value],
+                                                            acc[o - H0]);
+                                });
                             });
+                            if constexpr (bj + 1 < JB1) tmem_wait_ld(v[(bj + 1) & 1]);
                         });
-                    });
-                    int slot = (gs + ci * C::KB + C::R) % C::RING;
-                    float2 cs[C::KB];
+                        int slot = (gs + ci * C::KB + H0 + C::R) % C::RING;
+                        float2 cs[OR];
 #pragma unroll
-                    for (int o = 0; o < C::KB; ++o) {
-                        cs[o] = csring[slot * C::TX + lane];
-                        slot = (slot + 1 == C::RING) ? 0 : slot + 1;
-                    }
-                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                    mbar_arrive(&empty[q & 1]);
-                    if (active) {
+                        for (int o = 0; o < OR; ++o) {
+                            cs[o] = csring[slot * C::TX + lane];
+                            slot = (slot + 1 == C::RING) ? 0 : slot + 1;
+                        }
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        mbar_arrive(&empty[q & 1]);
+                        if (active && xok) {
+                            // Re[conj(H) blur] into the partial tile (each element is updated by
+                            // this thread only, in sample order)
 #pragma unroll
-                        for (int o = 0; o < C::KB; ++o)
-                            if (xok && cy + o < ty1)
-                                dst[(long long)o * a.W] = fmaf(cs[o].x, acc[o].x, fmaf(cs[o].y, acc[o].y, old[o]));
+                            for (int o = 0; o < OR; ++o)
+                                if (cy + o < ty1) {
+                                    dst[(long long)o * a.W] = fmaf(cs[o].x, acc[o].x, fmaf(cs[o].y, acc[o].y, old[o]));
+                                }
+                        }
                     }
                 }
+            };
+            if constexpr (C::CW == 1) {
+                body(std::integral_constant<int, 0>{});
+            } else {
+                if (h == 0) body(std::integral_constant<int, 0>{});
+                else body(std::integral_constant<int, 1>{});
             }
         }
     }

@@ -129,8 +129,7 @@ bf_status_t ensure_device(bf_vec_plan_t p) {
     BF_CUDA(cudaMalloc(&p->dQ, sizeof(double) * 64));
     BF_CUDA(cudaMalloc(&p->dgamma, sizeof(double) * 8));
     BF_CUDA(cudaMalloc(&p->ddiag, 16));
-    if (!fused_select(p->d, p->r, p->force_variant, &p->kinfo)) return BF_E_UNSUPPORTED;
-    p->kinfo_ok = true;
+    p->kinfo_ok = p->r <= kMaxR && fused_select(p->d, p->r, p->force_variant, &p->kinfo);
     p->device = dev;
     return BF_OK;
 }
@@ -249,6 +248,7 @@ bf_status_t encode_tmap(CUtensorMap *map, float *base, int dp, int Wp, int Hp, i
 // one fused launch: output rows [out_row0, out_row0+out_rows), samples [k0, k1)
 bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_row0, int out_row0,
                       int out_rows, int k0, int k1, cudaStream_t s, int *groups_out) {
+    if (!p->kinfo_ok) return BF_E_UNSUPPORTED;   // r > 64 or no compiled instance: engine 1 only
     int tile_rows = 0, groups = 1;
     choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups);
     const KernelInfo &ki = p->kinfo;
@@ -306,6 +306,142 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
     return BF_OK;
 }
 
+// Separable spatial taps w(|m|), m in [-r, r], normalised to sum 1 in fp64 (reading R3) and
+// rounded once to fp32. Eq. (1) gives the Gaussian; PAPER.md:205 allows "any
+// arbitrary spatial filter (such as a box or hat filter)" (reading R15: same window r).
+void make_taps(bf_vec_plan_t p) {
+    const int r = p->r;
+    if (r > kMaxR) {                       // FIR / direct unsupported at this radius
+        for (int m = 0; m <= kMaxR; ++m) p->taps[m] = 0.f;
+        return;
+    }
+    double w[kMaxR + 1], sum = 0.0;
+    for (int m = 0; m <= r; ++m) {
+        if (p->spatial == 1) w[m] = 1.0;                                   // box
+        else if (p->spatial == 2) w[m] = (double)(r + 1 - m);              // hat
+        else w[m] = std::exp(-(double)m * m / (2.0 * p->sigma_s * p->sigma_s));   // Gaussian
+        sum += (m == 0 ? 1.0 : 2.0) * w[m];
+    }
+    for (int m = 0; m <= kMaxR; ++m) p->taps[m] = (m <= r) ? (float)(w[m] / sum) : 0.f;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Recursive engine (reading R16): Deriche's 4th-order recursive Gaussian
+// (PAPER.md:204). The plan computes, in fp64, the poles z_j = exp((-b_j + i w_j) / sigma_s),
+// the residues A_j = (a_j - i a'_j) / S normalised so that the kernel sums to one
+// (S = 2 Re sum_j A_j / (1 - z_j) - h(0), the closed-form sum of h(|m|) over all integers m),
+// and per axis of length n the reflected-periodic initial-state factors z^n and 1 / (1 - z^2n).
+// ---------------------------------------------------------------------------------------------
+struct Cplx {
+    double r, i;
+};
+Cplx cmul(Cplx a, Cplx b) { return {a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
+Cplx cdiv(Cplx a, Cplx b) {
+    const double den = b.r * b.r + b.i * b.i;
+    return {(a.r * b.r + a.i * b.i) / den, (a.i * b.r - a.r * b.i) / den};
+}
+Cplx cexp_(double re, double im) { return {std::exp(re) * std::cos(im), std::exp(re) * std::sin(im)}; }
+
+void rec_axis(double sigma, int n, RecAxis *ax) {
+    // Deriche (1993) smoothing constants: h(x) = (a0 cos(w0 x/s) + a1 sin(w0 x/s)) e^{-b0 x/s}
+    //                                           + (c0 cos(w1 x/s) + c1 sin(w1 x/s)) e^{-b1 x/s}
+    const double a0 = 1.68, a1 = 3.735, b0 = 1.783, b1 = 1.723, c0 = -0.6803, c1 = -0.2598, w0 = 0.6318,
+                 w1 = 1.997;
+    const double bj[2] = {b0, b1}, wj[2] = {w0, w1};
+    const Cplx Aj[2] = {{a0, -a1}, {c0, -c1}};
+    Cplx z[2];
+    double S = -(a0 + c0);
+    for (int j = 0; j < 2; ++j) {
+        z[j] = cexp_(-bj[j] / sigma, wj[j] / sigma);
+        S += 2.0 * cdiv(Aj[j], Cplx{1.0 - z[j].r, -z[j].i}).r;
+    }
+    for (int j = 0; j < 2; ++j) {
+        ax->zr[j] = (float)z[j].r;
+        ax->zi[j] = (float)z[j].i;
+        ax->ar[j] = (float)(Aj[j].r / S);
+        ax->ai[j] = (float)(Aj[j].i / S);
+        const Cplx zn = cexp_(-bj[j] * n / sigma, wj[j] * n / sigma);
+        const Cplx inv = cdiv(Cplx{1.0, 0.0}, Cplx{1.0 - cmul(zn, zn).r, -cmul(zn, zn).i});
+        ax->znr[j] = (float)zn.r;
+        ax->zni[j] = (float)zn.i;
+        ax->invr[j] = (float)inv.r;
+        ax->invi[j] = (float)inv.i;
+    }
+    ax->g0 = (float)((a0 + c0) / S);
+    // head / tail terms above 2^-30: |z|^m = e^{-min(b) m / sigma}
+    const double lh = std::ceil(30.0 * std::log(2.0) * sigma / std::min(b0, b1));
+    ax->lh = (int)std::min<double>(n, lh);
+}
+
+bf_status_t ensure_rec_scratch(bf_vec_plan_t p, int nb) {
+    const size_t per = sizeof(float) * (size_t)2 * (p->d + 1) * p->H * (size_t)p->W;
+    if (p->drec_bytes < 2 * per * nb) {
+        cudaFree(p->drec);
+        p->drec = nullptr;
+        p->drec_bytes = 0;
+        BF_CUDA(cudaMalloc(&p->drec, 2 * per * nb));
+        p->drec_bytes = 2 * per * nb;
+    }
+    return BF_OK;
+}
+
+// samples [k0, k1) of the recursive engine into p->dpz (groups = samples per batch)
+bf_status_t run_recursive(bf_vec_plan_t p, const float *f, int k0, int k1, cudaStream_t s, int *groups_out) {
+    const int ns = k1 - k0;
+    const size_t px = (size_t)p->H * p->W;
+    // per sample in flight: y1 + y2 (2 x 2(d+1) planes) + one partial group ((d+1) planes)
+    const double per = 4.0 * px * (4.0 * (p->d + 1) + (p->d + 1));
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+    cudaGetLastError();
+    int nb = (int)std::max(1.0, std::min<double>(16.0, 0.4 * (free_b + p->drec_bytes + p->pz_bytes) / per));
+    if (p->force_batch > 0) nb = p->force_batch;
+    nb = std::min(nb, ns);
+    bf_status_t st = ensure_rec_scratch(p, nb);
+    if (st != BF_OK) return st;
+    st = ensure_pz(p, sizeof(float) * (size_t)nb * (p->d + 1) * px);
+    if (st != BF_OK) return st;
+    RecArgs a;
+    std::memset(&a, 0, sizeof(a));
+    fill_mu(p);
+    a.f = f;
+    a.t = p->dt;
+    a.y1 = p->drec;
+    a.y2 = p->drec + (size_t)nb * 2 * (p->d + 1) * px;
+    a.pz = p->dpz;
+    for (int c = 0; c < kMaxD; ++c) a.mu[c] = p->mu[c];
+    a.d = p->d;
+    a.H = p->H;
+    a.W = p->W;
+    rec_axis(p->sigma_s, p->W, &a.row);
+    rec_axis(p->sigma_s, p->H, &a.col);
+    int slot = -1;
+    if (p->profile) {
+        if (p->ev_count == bf_vec_plan_s::kEvRing) collect_profile(p);
+        slot = p->ev_head;
+        for (int j = 0; j < 2; ++j)
+            if (!p->ev[slot][j]) BF_CUDA(cudaEventCreate(&p->ev[slot][j]));
+        BF_CUDA(cudaEventRecord(p->ev[slot][0], s));
+    }
+    for (int kb = k0; kb < k1; kb += nb) {
+        a.k0 = kb;
+        a.nb = std::min(nb, k1 - kb);
+        a.first = (kb == k0) ? 1 : 0;
+        BF_CUDA(launch_recursive(a, s));
+    }
+    if (slot >= 0) {
+        BF_CUDA(cudaEventRecord(p->ev[slot][1], s));
+        p->ev_head = (p->ev_head + 1) % bf_vec_plan_s::kEvRing;
+        p->ev_count += 1;
+    }
+    p->last_batch = nb;
+    p->last_groups = nb;
+    p->last_tile_rows = p->H;
+    p->last_ctas = (long long)((p->H + 31) / 32 + (p->W + 31) / 32) * nb;
+    *groups_out = nb;
+    return BF_OK;
+}
+
 bool valid_plan(bf_vec_plan_t p) { return p != nullptr; }
 
 }  // namespace
@@ -335,7 +471,7 @@ bf_status_t bf_vec_plan(int H, int W, int d, double sigma_s, const double *C, in
     if (!(sigma_s > 0.0) || !std::isfinite(sigma_s)) return BF_E_ARG;
     if (N < 2 || N > 64 || (N & 1)) return BF_E_ARG;
     const int r = (int)std::ceil(3.0 * sigma_s - 1e-12);   // reading R2
-    if (r < 1 || r > kMaxR) return BF_E_ARG;
+    if (r < 1 || r > kMaxRec) return BF_E_ARG;
     bf_vec_plan_t p = new (std::nothrow) bf_vec_plan_s();
     if (!p) return BF_E_ARG;
     p->H = H; p->W = W; p->d = d; p->N = N; p->M = M; p->r = r;
@@ -344,13 +480,7 @@ bf_status_t bf_vec_plan(int H, int W, int d, double sigma_s, const double *C, in
     std::memcpy(p->C, C, sizeof(double) * d * d);
     bf_status_t st = diagonalize(d, C, p->Q, p->alpha);
     if (st != BF_OK) { delete p; return st; }
-    // Eq. (1) spatial taps, normalised in fp64 (reading R3), rounded once to fp32
-    double w[kMaxR + 1], sum = 0.0;
-    for (int m = 0; m <= r; ++m) {
-        w[m] = std::exp(-(double)m * m / (2.0 * sigma_s * sigma_s));
-        sum += (m == 0 ? 1.0 : 2.0) * w[m];
-    }
-    for (int m = 0; m <= kMaxR; ++m) p->taps[m] = (m <= r) ? (float)(w[m] / sum) : 0.f;
+    make_taps(p);
     // alias warning (reading R14): (pi/2) sqrt(N) < alpha_c R ||q_c||_1
     p->alias = false;
     for (int c = 0; c < d; ++c) {
@@ -369,7 +499,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         if (p->last) cudaStreamSynchronize(p->last);
         cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
-        cudaFree(p->dhost_in); cudaFree(p->dhost_out);
+        cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec);
         for (auto &pair : p->ev)
             for (auto &e : pair)
                 if (e) cudaEventDestroy(e);
@@ -408,12 +538,21 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
                                int row0, int row1, float *out, cudaStream_t s) {
     if (!p->sampled) return BF_E_STATE;
     int groups = 1;
-    bf_status_t st = run_fused(p, slab, slab_rows, slab_row0, row0, row1 - row0, 0, p->M, s, &groups);
+    int D = p->kinfo.D;
+    bf_status_t st;
+    if (p->engine == 1) {
+        // the recursion runs along whole columns: full images only (no band sharding)
+        if (row0 != 0 || row1 != p->H || slab_row0 != 0 || slab_rows != p->H) return BF_E_UNSUPPORTED;
+        st = run_recursive(p, slab, 0, p->M, s, &groups);
+        D = p->d;
+    } else {
+        st = run_fused(p, slab, slab_rows, slab_row0, row0, row1 - row0, 0, p->M, s, &groups);
+    }
     if (st != BF_OK) return st;
     BF_CUDA(launch_diag_reset(p->ddiag, s));
-    BF_CUDA(launch_normalize_groups(p->dpz, groups, p->kinfo.D, p->d, row1 - row0, p->W, p->mu, out,
+    BF_CUDA(launch_normalize_groups(p->dpz, groups, D, p->d, row1 - row0, p->W, p->mu, out,
                                     p->ddiag, 1.0f / p->M, (float)p->z_floor, s));
-    p->last_launches = 4;
+    p->last_launches = (p->engine == 1) ? 2 + 2 * ((p->M + p->last_batch - 1) / p->last_batch) : 4;
     p->last = s;
     return p->alias ? BF_W_ALIAS : BF_OK;
 }
@@ -456,9 +595,11 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k
         return BF_OK;
     }
     int groups = 1;
-    bf_status_t st = run_fused(p, f, p->H, 0, 0, p->H, k0, k1, s, &groups);
+    bf_status_t st = (p->engine == 1) ? run_recursive(p, f, k0, k1, s, &groups)
+                                      : run_fused(p, f, p->H, 0, 0, p->H, k0, k1, s, &groups);
     if (st != BF_OK) return st;
-    BF_CUDA(launch_finalize_partial(p->dpz, groups, p->kinfo.D, p->d, p->H, p->W, p->mu, rows_per_band, PZ, s));
+    BF_CUDA(launch_finalize_partial(p->dpz, groups, p->engine == 1 ? p->d : p->kinfo.D, p->d, p->H, p->W, p->mu,
+                                    rows_per_band, PZ, s));
     p->last_launches = 3;
     p->last = s;
     return BF_OK;
@@ -499,6 +640,7 @@ bf_status_t bf_vec_filter_rows(bf_vec_plan_t p, const float *slab, int slab_row0
 
 bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *stream) {
     if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
+    if (p->r > kMaxR) return BF_E_UNSUPPORTED;
     bf_status_t st = ensure_device(p);
     if (st != BF_OK) return st;
     const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
@@ -555,13 +697,25 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
     if (!std::strcmp(name, "tile_rows")) { if (v < 0) return BF_E_ARG; p->force_tile_rows = (int)v; return BF_OK; }
     if (!std::strcmp(name, "groups")) { if (v < 0) return BF_E_ARG; p->force_groups = (int)v; return BF_OK; }
     if (!std::strcmp(name, "variant")) {
-        if (v < 0 || v > 2) return BF_E_ARG;
+        if (v < 0 || v > 3) return BF_E_ARG;
         p->force_variant = (int)v;
         if (p->device >= 0) {   // re-select the kernel instance
             bfvec::KernelInfo ki;
             if (!fused_select(p->d, p->r, p->force_variant, &ki)) return BF_E_UNSUPPORTED;
             p->kinfo = ki;
         }
+        return BF_OK;
+    }
+    if (!std::strcmp(name, "engine")) {
+        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        p->engine = (int)v;
+        return BF_OK;
+    }
+    if (!std::strcmp(name, "rec_batch")) { if (v < 0) return BF_E_ARG; p->force_batch = (int)v; return BF_OK; }
+    if (!std::strcmp(name, "spatial_kernel")) {
+        if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
+        p->spatial = (int)v;
+        make_taps(p);
         return BF_OK;
     }
     if (!std::strcmp(name, "profile")) {
@@ -588,6 +742,8 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
+        {"spatial_kernel", p->spatial}, {"engine", p->engine}, {"rec_batch", p->last_batch},
+        {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)
         if (!std::strcmp(e.n, name)) { *value = e.v; return BF_OK; }

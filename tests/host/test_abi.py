@@ -63,7 +63,7 @@ def test_plan_validation_errors():
     C = np.eye(3) * 100.0
     for args in [(0, 8, 3, 1.0, C, 10, 4, 0), (8, 8, 3, 0.0, C, 10, 4, 0), (8, 8, 3, 1.0, C, 11, 4, 0),
                  (8, 8, 3, 1.0, C, 10, 0, 0), (8, 8, 9, 1.0, np.eye(9), 10, 4, 0),
-                 (8, 8, 3, 30.0, C, 10, 4, 0)]:
+                 (8, 8, 3, 4e5, C, 10, 4, 0)]:
         with pytest.raises(BfVecError):
             Plan(*args)
     with pytest.raises(BfVecError) as e:
@@ -87,3 +87,24 @@ def test_alias_warning_static():
     # alpha R = 255/30 = 8.5 > (pi/2) sqrt(4) = 3.14 -> aliasing; N = 40 -> 9.93 > 8.5: fine
     assert Plan(8, 8, 1, 1.0, [[900.0]], 4, 4, 0).info("alias") == 1
     assert Plan(8, 8, 1, 1.0, [[900.0]], 40, 4, 0).info("alias") == 0
+
+
+def test_large_radius_plan_is_recursive_only():
+    """r = ceil(3 sigma_s) > 64: the plan is valid (the recursive engine runs it) but the
+    truncated-window engine reports itself unsupported."""
+    from paper_1605_02164_b200 import Plan
+    p = Plan(16, 16, 3, 30.0, np.eye(3) * 100.0, 10, 4, 0)
+    assert p.info("radius") == 90 and p.info("fir_supported") == 0
+    p.set_option("engine", 1)
+    assert p.info("engine") == 1
+    assert Plan(16, 16, 3, 2.0, np.eye(3) * 100.0, 10, 4, 0).info("fir_supported") == 1
+
+
+def test_options_validate_without_gpu():
+    from paper_1605_02164_b200 import BfVecError, Plan
+    p = Plan(16, 16, 3, 2.0, np.eye(3) * 100.0, 10, 4, 0)
+    for name, v in [("engine", 1), ("engine", 0), ("spatial_kernel", 2), ("rec_batch", 3)]:
+        p.set_option(name, v)
+    for name, v in [("engine", 2), ("spatial_kernel", 5), ("rec_batch", -1), ("no_such_option", 1)]:
+        with pytest.raises(BfVecError):
+            p.set_option(name, v)

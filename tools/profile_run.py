@@ -19,8 +19,14 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--samples", type=int, default=0)
 ap.add_argument("--tile-rows", type=int, default=0)
 ap.add_argument("--groups", type=int, default=0)
+ap.add_argument("--variant", type=int, default=0)
+ap.add_argument("--engine", type=int, default=0)
+ap.add_argument("--sigma", type=float, default=0.0, help="override sigma_s (recursive engine sweeps)")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
+if a.sigma:
+    import dataclasses
+    cfg = dataclasses.replace(cfg, sigma_s=a.sigma)
 rows = a.rows or cfg.H
 y0 = (cfg.H - rows) // 2
 s0, s1 = native.slab_bounds(cfg.H, y0, rows, cfg.radius)
@@ -31,6 +37,10 @@ if a.tile_rows:
     p.set_option('tile_rows', a.tile_rows)
 if a.groups:
     p.set_option('groups', a.groups)
+if a.variant:
+    p.set_option('variant', a.variant)
+if a.engine:
+    p.set_option('engine', a.engine)
 slab = torch.from_numpy(make_image_rows(cfg, s0, s1)).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for i in range(a.reps):
