@@ -154,6 +154,24 @@ bf_status_t bf_vec_filter_rows(bf_vec_plan_t plan, const float *slab, int slab_r
 bf_status_t bf_vec_direct(bf_vec_plan_t plan, const float *f, float *out, void *stream);
 
 /*
+ * bf_vec_mse_sweep -- the error-vs-T experiment of PAPER.md:271-282 (Fig. 5) on the device:
+ * for each realisation r (the sampler keyed by seeds[r] instead of the plan seed, reading R9)
+ * and each checkpoint T_j of t_list, the MC filter over the first T_j samples is compared with
+ * a reference image and
+ *     mse[r * n_t + j] = 1/(d |Omega|) sum_c sum_i (ref_c(i) - S_c(i))^2        (Eq. (20))
+ * is written (host, double). Samples are shared between checkpoints (T_j extends T_{j-1}).
+ *   f, ref     device planar (d, H, W) float32 (ref: usually bf_vec_direct's output)
+ *   seeds      host, n_seeds keys;  t_list  host, n_t strictly increasing values in [1, M]
+ *   mse        host, n_seeds x n_t doubles
+ * Synchronous on `stream`; restores the plan's own draws before returning. Uses the plan's
+ * engine, spatial kernel and sampler options. Errors: BF_E_ARG, BF_E_STATE (sample_freqs
+ * not called), BF_E_UNSUPPORTED, BF_E_CUDA.
+ */
+bf_status_t bf_vec_mse_sweep(bf_vec_plan_t plan, const float *f, const float *ref, int n_seeds,
+                             const uint64_t *seeds, int n_t, const int *t_list, double *mse,
+                             void *stream);
+
+/*
  * bf_vec_diag -- synchronises the plan's last stream and returns diagnostics of
  * the most recent filter/normalize call: z_min = min over pixels of Z/M and
  * n_small_z = #pixels with Z/M < z_floor (default 0.05). Returns BF_W_SMALL_Z

@@ -165,6 +165,20 @@ class Plan:
               "bf_vec_direct")
         return out
 
+    def mse_sweep(self, f, ref, seeds, t_list, stream=None):
+        """bf_vec_mse_sweep: (len(seeds), len(t_list)) array of Eq. (20) MSEs between ref and the
+        MC filter over the first T samples of realisation seeds[r] (Fig. 5)."""
+        shp = (self.d, self.H, self.W)
+        sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        tl = np.ascontiguousarray(np.asarray(t_list, dtype=np.int32))
+        out = np.empty((len(sd), len(tl)), dtype=np.float64)
+        check(self._lib.bf_vec_mse_sweep(self._h, _dev(f, shp, "f"), _dev(ref, shp, "ref"), len(sd),
+                                         sd.ctypes.data_as(ctypes.c_void_p), len(tl),
+                                         tl.ctypes.data_as(ctypes.c_void_p),
+                                         out.ctypes.data_as(ctypes.c_void_p), _stream_ptr(stream)),
+              "bf_vec_mse_sweep")
+        return out
+
     def diag(self):
         zm = ctypes.c_float()
         n = ctypes.c_longlong()

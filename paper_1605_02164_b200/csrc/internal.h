@@ -99,6 +99,14 @@ struct RecArgs {
 };
 cudaError_t launch_recursive(const RecArgs &a, cudaStream_t s);
 
+// Error-vs-T sweep (sweep.cu): fold partial groups into running (P', Z), S = P'/Z + mu,
+// accumulate sum (ref - S)^2 into *out (double).
+struct MuArg {
+    float v[kMaxD];
+};
+cudaError_t launch_mse_accum(const float *pz, int groups, int D, int d, long long npix, const float *mu,
+                             float *run, int first, const float *ref, double *out, cudaStream_t s);
+
 // Direct filter (direct.cu)
 cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const float *w,
                           const float *A /* d x d: diag(alpha) Q^T scaled */, float *U,
@@ -125,6 +133,10 @@ struct bf_vec_plan_s {
     int engine = 0;            // 0 truncated FIR (Eq. (1) window), 1 recursive Deriche (reading R16)
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
     float *drec = nullptr;     // recursive engine scratch (y1, y2)
+    float *drun = nullptr;     // error sweep: running (P', Z) planes and per-checkpoint sums
+    double *dmse = nullptr;
+    size_t drun_bytes = 0;
+    int dmse_n = 0;
     size_t drec_bytes = 0;
     int last_batch = 0;
     // device state (lazily created)

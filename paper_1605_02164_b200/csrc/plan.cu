@@ -499,7 +499,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         if (p->last) cudaStreamSynchronize(p->last);
         cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
-        cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec);
+        cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drun); cudaFree(p->dmse);
         for (auto &pair : p->ev)
             for (auto &e : pair)
                 if (e) cudaEventDestroy(e);
@@ -661,6 +661,56 @@ bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *str
     p->last_launches = 2;
     p->last = s;
     return BF_OK;
+}
+
+bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, int n_seeds, const uint64_t *seeds,
+                             int n_t, const int *t_list, double *mse, void *stream) {
+    if (!valid_plan(p) || !f || !ref || !seeds || !t_list || !mse || n_seeds < 1 || n_t < 1) return BF_E_ARG;
+    for (int j = 0; j < n_t; ++j)
+        if (t_list[j] < 1 || t_list[j] > p->M || (j > 0 && t_list[j] <= t_list[j - 1])) return BF_E_ARG;
+    if (p->device < 0 || !p->sampled) return BF_E_STATE;
+    cudaStream_t s = S(stream);
+    const long long npix = (long long)p->H * p->W;
+    const size_t run_bytes = sizeof(float) * (size_t)(p->d + 1) * npix;
+    if (p->drun_bytes < run_bytes) {
+        cudaFree(p->drun);
+        p->drun = nullptr;
+        p->drun_bytes = 0;
+        BF_CUDA(cudaMalloc(&p->drun, run_bytes));
+        p->drun_bytes = run_bytes;
+    }
+    if (p->dmse_n < n_t) {
+        cudaFree(p->dmse);
+        p->dmse = nullptr;
+        p->dmse_n = 0;
+        BF_CUDA(cudaMalloc(&p->dmse, sizeof(double) * n_t));
+        p->dmse_n = n_t;
+    }
+    bf_status_t st = BF_OK;
+    for (int r = 0; r < n_seeds && st == BF_OK; ++r) {
+        // realisation r: the same generator keyed by seeds[r] (reading R9)
+        BF_CUDA(launch_sampler(p->M, p->d, p->N, seeds[r], p->dQ, p->dgamma, p->dX, p->dt, s));
+        BF_CUDA(cudaMemsetAsync(p->dmse, 0, sizeof(double) * n_t, s));
+        int k0 = 0;
+        for (int j = 0; j < n_t && st == BF_OK; ++j) {
+            int groups = 1;
+            st = (p->engine == 1) ? run_recursive(p, f, k0, t_list[j], s, &groups)
+                                  : run_fused(p, f, p->H, 0, 0, p->H, k0, t_list[j], s, &groups);
+            if (st != BF_OK) break;
+            BF_CUDA(launch_mse_accum(p->dpz, groups, p->engine == 1 ? p->d : p->kinfo.D, p->d, npix, p->mu, p->drun,
+                                     j == 0 ? 1 : 0, ref, p->dmse + j, s));
+            k0 = t_list[j];
+        }
+        if (st != BF_OK) break;
+        BF_CUDA(cudaMemcpyAsync(mse + (size_t)r * n_t, p->dmse, sizeof(double) * n_t, cudaMemcpyDeviceToHost, s));
+        BF_CUDA(cudaStreamSynchronize(s));
+        for (int j = 0; j < n_t; ++j) mse[(size_t)r * n_t + j] /= (double)p->d * (double)npix;   // Eq. (20)
+    }
+    // restore the plan's own draws
+    BF_CUDA(launch_sampler(p->M, p->d, p->N, p->seed, p->dQ, p->dgamma, p->dX, p->dt, s));
+    p->last = s;
+    p->last_launches = 0;
+    return st;
 }
 
 bf_status_t bf_vec_diag(bf_vec_plan_t p, float *z_min, long long *n_small_z) {
