@@ -197,6 +197,12 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 §11). Engine 1 filters whole images only (bf_vec_filter, _host, _partial;
  *                 bf_vec_filter_rows returns BF_E_UNSUPPORTED for a proper band) and ignores
  *                 "spatial_kernel", "variant", "tile_rows" and "groups".
+ *   "sampler"     frequency draws of the next bf_vec_sample_freqs / bf_vec_mse_sweep:
+ *                 0 (default) iid X ~ B(N, 1/2) by popcount (reading R9); 1 stratified: per
+ *                 dimension a Latin-hypercube stratification of the binomial CDF over the M
+ *                 samples (each stratum [j/M, (j+1)/M) used once, random order; DESIGN.md
+ *                 reading R17; the paper's "improving the Monte Carlo integration",
+ *                 PAPER.md:313). Same estimator Eq. (14); X still B(N, 1/2)-distributed.
  *   "rec_batch"   engine 1: samples per batch (0 = auto from free device memory; each sample
  *                 in flight holds 5 (d+1) fp32 planes of H x W scratch)
  *   "spatial_kernel" separable spatial taps on the window [-r, r], r = ceil(3 sigma_s):
@@ -216,7 +222,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value
  *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
  *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
  *   "regs", "occupancy", "alias", "variant", "spatial_kernel", "engine", "rec_batch" (last batch
- *   size), "fir_supported" (r <= 64), and (option "profile") "fused_ns_total",
+ *   size), "fir_supported" (r <= 64), "sampler", and (option "profile") "fused_ns_total",
  *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
  *   an unknown name.
  */

@@ -19,13 +19,15 @@ def mse(B, S):
     return float(np.mean((B - S) ** 2))
 
 
-def mse_curve(f, ref, Q, alpha, N, seeds, t_list, sigma_s, spatial="gaussian"):
-    """(len(seeds), len(t_list)) MSEs; realisation r uses y_draws(seeds[r], max T, d, N) and
-    checkpoint j its first t_list[j] draws (Alg. 1 run afresh on each prefix)."""
+def mse_curve(f, ref, Q, alpha, N, seeds, t_list, sigma_s, spatial="gaussian", sampler="iid", M=None):
+    """(len(seeds), len(t_list)) MSEs; realisation r draws M (default max T) samples with
+    seeds[r] (iid: reading R9, stratified over the M strata: reading R17) and checkpoint j uses
+    the first t_list[j] of them (Alg. 1 run afresh on each prefix)."""
     d = f.shape[0]
+    M = int(max(t_list)) if M is None else int(M)
     out = np.empty((len(seeds), len(t_list)))
     for r, s in enumerate(seeds):
-        Y = draws.y_draws(int(s), int(max(t_list)), d, N)
+        Y = (draws.y_draws if sampler == "iid" else draws.stratified_y_draws)(int(s), M, d, N)
         for j, T in enumerate(t_list):
             S, _, _ = native.mcsf_full(f, Q, alpha, N, Y[:T], sigma_s, spatial=spatial)
             out[r, j] = mse(ref, S)

@@ -63,6 +63,11 @@ cudaError_t launch_pad(const float *f, long long plane, int d, int H, int W, int
 cudaError_t launch_sampler(int M, int d, int N, uint64_t seed, const double *dQ,
                            const double *dgamma, int32_t *dX, float *dt, cudaStream_t s);
 void philox4x64_10_host(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]);
+struct CumTable {
+    uint64_t v[65];   // cum(n) = sum_{m <= n} C(N, m) for n < N (all-ones beyond)
+};
+cudaError_t launch_sampler_stratified(int M, int d, int N, uint64_t seed, const double *dQ, const double *dgamma,
+                                      uint64_t *dkeys, int32_t *dX, float *dt, cudaStream_t s);
 
 // Epilogues (normalize.cu)
 cudaError_t launch_normalize_groups(const float *pz, int groups, int D, int d, int rows, int W,
@@ -133,6 +138,8 @@ struct bf_vec_plan_s {
     int engine = 0;            // 0 truncated FIR (Eq. (1) window), 1 recursive Deriche (reading R16)
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
     float *drec = nullptr;     // recursive engine scratch (y1, y2)
+    int sampler = 0;           // 0 iid binomial draws (reading R9), 1 stratified (reading R17)
+    uint64_t *dkeys = nullptr; // stratified sampler: permutation keys (M d)
     float *drun = nullptr;     // error sweep: running (P', Z) planes and per-checkpoint sums
     double *dmse = nullptr;
     size_t drun_bytes = 0;

@@ -442,6 +442,17 @@ bf_status_t run_recursive(bf_vec_plan_t p, const float *f, int k0, int k1, cudaS
     return BF_OK;
 }
 
+// the plan's draw set for key `seed` (iid or stratified, option "sampler")
+bf_status_t draw(bf_vec_plan_t p, uint64_t seed, cudaStream_t s) {
+    if (p->sampler == 1) {
+        if (!p->dkeys) BF_CUDA(cudaMalloc(&p->dkeys, sizeof(uint64_t) * (size_t)p->M * p->d));
+        BF_CUDA(launch_sampler_stratified(p->M, p->d, p->N, seed, p->dQ, p->dgamma, p->dkeys, p->dX, p->dt, s));
+    } else {
+        BF_CUDA(launch_sampler(p->M, p->d, p->N, seed, p->dQ, p->dgamma, p->dX, p->dt, s));
+    }
+    return BF_OK;
+}
+
 bool valid_plan(bf_vec_plan_t p) { return p != nullptr; }
 
 }  // namespace
@@ -500,6 +511,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
         cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drun); cudaFree(p->dmse);
+        cudaFree(p->dkeys);
         for (auto &pair : p->ev)
             for (auto &e : pair)
                 if (e) cudaEventDestroy(e);
@@ -515,7 +527,8 @@ bf_status_t bf_vec_sample_freqs(bf_vec_plan_t p, void *stream) {
     for (int c = 0; c < p->d; ++c) gamma[c] = p->alpha[c] / std::sqrt((double)p->N);
     BF_CUDA(cudaMemcpy(p->dQ, p->Q, sizeof(double) * p->d * p->d, cudaMemcpyHostToDevice));
     BF_CUDA(cudaMemcpy(p->dgamma, gamma, sizeof(double) * p->d, cudaMemcpyHostToDevice));
-    BF_CUDA(launch_sampler(p->M, p->d, p->N, p->seed, p->dQ, p->dgamma, p->dX, p->dt, S(stream)));
+    st = draw(p, p->seed, S(stream));
+    if (st != BF_OK) return st;
     p->sampled = true;
     p->last = S(stream);
     return BF_OK;
@@ -689,7 +702,8 @@ bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, 
     bf_status_t st = BF_OK;
     for (int r = 0; r < n_seeds && st == BF_OK; ++r) {
         // realisation r: the same generator keyed by seeds[r] (reading R9)
-        BF_CUDA(launch_sampler(p->M, p->d, p->N, seeds[r], p->dQ, p->dgamma, p->dX, p->dt, s));
+        st = draw(p, seeds[r], s);
+        if (st != BF_OK) break;
         BF_CUDA(cudaMemsetAsync(p->dmse, 0, sizeof(double) * n_t, s));
         int k0 = 0;
         for (int j = 0; j < n_t && st == BF_OK; ++j) {
@@ -707,9 +721,10 @@ bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, 
         for (int j = 0; j < n_t; ++j) mse[(size_t)r * n_t + j] /= (double)p->d * (double)npix;   // Eq. (20)
     }
     // restore the plan's own draws
-    BF_CUDA(launch_sampler(p->M, p->d, p->N, p->seed, p->dQ, p->dgamma, p->dX, p->dt, s));
+    const bf_status_t st2 = draw(p, p->seed, s);
     p->last = s;
     p->last_launches = 0;
+    if (st == BF_OK) st = st2;
     return st;
 }
 
@@ -761,6 +776,11 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         p->engine = (int)v;
         return BF_OK;
     }
+    if (!std::strcmp(name, "sampler")) {
+        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        p->sampler = (int)v;   // takes effect at the next bf_vec_sample_freqs
+        return BF_OK;
+    }
     if (!std::strcmp(name, "rec_batch")) { if (v < 0) return BF_E_ARG; p->force_batch = (int)v; return BF_OK; }
     if (!std::strcmp(name, "spatial_kernel")) {
         if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
@@ -792,7 +812,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"engine", p->engine}, {"rec_batch", p->last_batch},
+        {"spatial_kernel", p->spatial}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"sampler", p->sampler},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)

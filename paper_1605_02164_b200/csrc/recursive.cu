@@ -94,15 +94,36 @@ __device__ __forceinline__ void init_state(const RecAxis &ax, const HeadSum &hd,
 // ---------------------------------------------------------------------------------------------
 // Row pass: CTA = 32 rows (lane = row) x NP warps (warp = (cos, sin) pair: Z, G_0 .. G_{d-1}) of
 // one sample. Chunks of 32 columns are staged through shared memory so every global access is
-// coalesced along x.
+// coalesced along x; the next chunk's f tile (and, in the backward sweep, its partial tile) is
+// prefetched with cp.async while the current chunk's recursions run.
 // ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async4(float *dst, const float *src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(valid ? 4 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NP>
+struct RowSmem {
+    static constexpr int D = NP - 1;
+    static constexpr int TILE = kT * (kT + 1);           // floats per padded 32 x 32 tile
+    static constexpr int OB = (NP <= 6) ? 2 : 1;         // partial-tile buffers (227 KB budget)
+    static constexpr int OFF_CS = 2 * D * TILE;          // fs[2][D] tiles first
+    static constexpr int OFF_OB = OFF_CS + 2 * TILE;     // cs: TILE float2
+    static constexpr size_t BYTES = sizeof(float) * (size_t)(OFF_OB + OB * 2 * NP * TILE);
+};
+
 template <int NP>
 __global__ void __launch_bounds__(32 * NP) rec_row_kernel(const __grid_constant__ RecArgs a) {
-    constexpr int D = NP - 1;
+    using L = RowSmem<NP>;
+    constexpr int D = L::D, TILE = L::TILE;
     extern __shared__ float sm[];
-    float(*fs)[kT][kT + 1] = reinterpret_cast<float(*)[kT][kT + 1]>(sm);               // [D][32][33] f - mu
-    float2(*cs)[kT + 1] = reinterpret_cast<float2(*)[kT + 1]>(sm + D * kT * (kT + 1));   // [32][33] (c, s)
-    float(*ot)[kT][kT + 1] = reinterpret_cast<float(*)[kT][kT + 1]>(sm + (D + 2) * kT * (kT + 1));  // [2NP][32][33]
+    auto fs = [&](int buf, int c) { return sm + (buf * D + c) * TILE; };          // [32][33] f - mu
+    float2(*cs)[kT + 1] = reinterpret_cast<float2(*)[kT + 1]>(sm + L::OFF_CS);      // [32][33] (c, s)
+    auto ob = [&](int buf, int q) { return sm + L::OFF_OB + (buf * 2 * NP + q) * TILE; };
 
     const int tid = threadIdx.x, lane = tid & 31, p = tid >> 5;
     const int y0 = blockIdx.x * kT;
@@ -117,31 +138,55 @@ __global__ void __launch_bounds__(32 * NP) rec_row_kernel(const __grid_constant_
     const RecAxis &ax = a.row;
     const int nchunk = (W + kT - 1) / kT;
 
-    // stage f (centred) and the modulation (c, s) of chunk cx
-    auto load_mod = [&](int cx) {
+    // cp.async the raw f tile of chunk cx into fs(buf, .) (zeros outside the image)
+    auto issue_f = [&](int cx, int buf) {
         const int x0 = cx * kT;
         for (int e = tid; e < D * kT * kT; e += 32 * NP) {
             const int c = e / (kT * kT), i = (e / kT) % kT, j = e % kT;
             const int x = x0 + j, y = y0 + i;
-            fs[c][i][j] = (x < W && y < H) ? a.f[c * plane + (long long)y * W + x] - a.mu[c] : 0.f;
+            const bool ok = x < W && y < H;
+            cp_async4(fs(buf, c) + i * (kT + 1) + j, ok ? a.f + c * plane + (long long)y * W + x : a.f, ok);
         }
-        __syncthreads();
+    };
+    auto issue_y1 = [&](int cx, int buf) {
+        const int x0 = cx * kT;
+        for (int e = tid; e < 2 * NP * kT * kT; e += 32 * NP) {
+            const int q = e / (kT * kT), i = (e / kT) % kT, j = e % kT;
+            const int x = x0 + j, y = y0 + i;
+            const bool ok = x < W && y < H;
+            cp_async4(ob(buf, q) + i * (kT + 1) + j, ok ? y1 + q * plane + (long long)y * W + x : y1, ok);
+        }
+    };
+    // centre f (reading R12) and form (c, s) = (cos, sin)(t_k . (f - mu)) of the staged tile
+    auto modulate = [&](int buf) {
         for (int e = tid; e < kT * kT; e += 32 * NP) {
             const int i = e / kT, j = e % kT;
             float th = 0.f;
 #pragma unroll
-            for (int c = 0; c < D; ++c) th = fmaf(tk[c], fs[c][i][j], th);
+            for (int c = 0; c < D; ++c) {
+                float *q = fs(buf, c) + i * (kT + 1) + j;
+                const float v = *q - a.mu[c];
+                *q = v;
+                th = fmaf(tk[c], v, th);
+            }
             float s, c;
             __sincosf(th, &s, &c);
             cs[i][j] = f2(c, s);
         }
-        __syncthreads();
     };
-    auto xval = [&](int i, int j) -> float2 {   // the pair's real input at (row i, column j)
+    auto xval = [&](int buf, int i, int j) -> float2 {   // the pair's real input at (row i, column j)
         const float2 h = cs[i][j];
         if (p == 0) return h;
-        const float fv = fs[p - 1][i][j];
+        const float fv = fs(buf, p - 1)[i * (kT + 1) + j];
         return f2(h.x * fv, h.y * fv);
+    };
+    auto stage_sync = [&](int cx) {   // synchronous staging (initial-state sums only)
+        issue_f(cx, 0);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        modulate(0);
+        __syncthreads();
     };
 
     // ---- reflected-periodic initial state: S_head (first Lh columns), S_tail (last Lh) ----
@@ -150,59 +195,92 @@ __global__ void __launch_bounds__(32 * NP) rec_row_kernel(const __grid_constant_
     tl.init();
     const int nh = min(W, ax.lh);
     for (int cx = 0; cx * kT < nh; ++cx) {
-        load_mod(cx);
-        for (int j = 0; j < kT && cx * kT + j < nh; ++j) hd.add(ax, xval(lane, j));
+        stage_sync(cx);
+        for (int j = 0; j < kT && cx * kT + j < nh; ++j) hd.add(ax, xval(0, lane, j));
         __syncthreads();
     }
     const int xt = W - nh;   // first column of the tail range
     for (int cx = nchunk - 1; cx >= 0 && (cx + 1) * kT > xt; --cx) {
         const int x0 = cx * kT;
-        load_mod(cx);
+        stage_sync(cx);
         for (int j = min(kT, W - x0) - 1; j >= 0; --j)
-            if (x0 + j >= xt) tl.add(ax, xval(lane, j));
+            if (x0 + j >= xt) tl.add(ax, xval(0, lane, j));
         __syncthreads();
     }
     Pole2 st;
     init_state(ax, hd, tl, st);
 
     // ---- forward sweep: y1 <- sum_j Re[A_j u_j] - g0 x ----
+    issue_f(0, 0);
+    cp_async_commit();
     for (int cx = 0; cx < nchunk; ++cx) {
+        const int buf = cx & 1;
         const int x0 = cx * kT;
         const int nj = min(kT, W - x0);
-        load_mod(cx);
+        if (cx + 1 < nchunk) {
+            issue_f(cx + 1, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        modulate(buf);
+        __syncthreads();
+        float *o0 = ob(0, 2 * p) + lane * (kT + 1), *o1 = ob(0, 2 * p + 1) + lane * (kT + 1);
         for (int j = 0; j < nj; ++j) {
-            const float2 x = xval(lane, j);
+            const float2 x = xval(buf, lane, j);
             step(ax, st, x);
             const float2 y = fma2s(-ax.g0, x, re_a(ax, st));
-            ot[2 * p][lane][j] = y.x;
-            ot[2 * p + 1][lane][j] = y.y;
+            o0[j] = y.x;
+            o1[j] = y.y;
         }
         __syncthreads();
         for (int e = tid; e < 2 * NP * kT * kT; e += 32 * NP) {
             const int q = e / (kT * kT), i = (e / kT) % kT, j = e % kT;
-            if (j < nj && y0 + i < H) y1[q * plane + (long long)(y0 + i) * W + x0 + j] = ot[q][i][j];
+            if (j < nj && y0 + i < H) y1[q * plane + (long long)(y0 + i) * W + x0 + j] = ob(0, q)[i * (kT + 1) + j];
         }
         __syncthreads();
     }
     // ---- backward sweep: v[n] = u[n-1]; y1 += sum_j Re[A_j v_j] ----
-    for (int cx = nchunk - 1; cx >= 0; --cx) {
+    issue_f(nchunk - 1, 0);
+    if (L::OB == 2) issue_y1(nchunk - 1, 0);
+    cp_async_commit();
+    for (int it = 0; it < nchunk; ++it) {
+        const int cx = nchunk - 1 - it;
+        const int buf = it & 1;
+        const int obuf = (L::OB == 2) ? buf : 0;
         const int x0 = cx * kT;
         const int nj = min(kT, W - x0);
-        for (int e = tid; e < 2 * NP * kT * kT; e += 32 * NP) {
-            const int q = e / (kT * kT), i = (e / kT) % kT, j = e % kT;
-            ot[q][i][j] = (j < nj && y0 + i < H) ? y1[q * plane + (long long)(y0 + i) * W + x0 + j] : 0.f;
+        if (it + 1 < nchunk) {
+            issue_f(cx - 1, buf ^ 1);
+            if (L::OB == 2) issue_y1(cx - 1, buf ^ 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
-        load_mod(cx);   // (its first __syncthreads also orders the ot loads)
+        if (L::OB == 1) {   // no room to prefetch the partial tile: plain coalesced loads
+            for (int e = tid; e < 2 * NP * kT * kT; e += 32 * NP) {
+                const int q = e / (kT * kT), i = (e / kT) % kT, j = e % kT;
+                ob(0, q)[i * (kT + 1) + j] =
+                    (j < nj && y0 + i < H) ? y1[q * plane + (long long)(y0 + i) * W + x0 + j] : 0.f;
+            }
+        }
+        __syncthreads();
+        modulate(buf);
+        __syncthreads();
+        float *o0 = ob(obuf, 2 * p) + lane * (kT + 1), *o1 = ob(obuf, 2 * p + 1) + lane * (kT + 1);
         for (int j = nj - 1; j >= 0; --j) {
-            step(ax, st, xval(lane, j));
+            step(ax, st, xval(buf, lane, j));
             const float2 y = re_a(ax, st);
-            ot[2 * p][lane][j] += y.x;
-            ot[2 * p + 1][lane][j] += y.y;
+            o0[j] += y.x;
+            o1[j] += y.y;
         }
         __syncthreads();
         for (int e = tid; e < 2 * NP * kT * kT; e += 32 * NP) {
             const int q = e / (kT * kT), i = (e / kT) % kT, j = e % kT;
-            if (j < nj && y0 + i < H) y1[q * plane + (long long)(y0 + i) * W + x0 + j] = ot[q][i][j];
+            if (j < nj && y0 + i < H) y1[q * plane + (long long)(y0 + i) * W + x0 + j] = ob(obuf, q)[i * (kT + 1) + j];
         }
         __syncthreads();
     }
@@ -269,7 +347,7 @@ __global__ void __launch_bounds__(32 * NP) rec_col_kernel(const __grid_constant_
 
 template <int NP>
 cudaError_t launch_np(const RecArgs &a, cudaStream_t s) {
-    const size_t smem = sizeof(float) * kT * (kT + 1) * ((NP - 1) + 2 + 2 * NP);
+    const size_t smem = RowSmem<NP>::BYTES;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(rec_row_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,

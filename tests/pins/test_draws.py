@@ -77,3 +77,43 @@ def test_determinism():
     b = draws.y_draws(3, 64, 8, 30)
     assert np.array_equal(a, b)
     assert not np.array_equal(a, draws.y_draws(4, 64, 8, 30))
+
+
+# ---- stratified draws (reading R17) ------------------------------------------------------------
+def test_stratified_reproduces_the_pmf_exactly_when_strata_align():
+    """M = 2^N strata: every CDF breakpoint cum(n)/2^N is a stratum edge, so each stratum maps to
+    one value and the counts are exactly C(N, n) (the binomial pmf times M)."""
+    import math
+    for N, d, seed in [(4, 2, 0), (6, 3, 1), (8, 1, 2)]:
+        X = draws.stratified_binomial_draws(seed, 2 ** N, d, N)
+        for c in range(d):
+            assert list(np.bincount(X[:, c], minlength=N + 1)) == [math.comb(N, n) for n in range(N + 1)]
+
+
+def test_stratified_counts_within_one_of_expected_and_strata_are_a_permutation():
+    import math
+    N, M, d = 40, 512, 3
+    X = draws.stratified_binomial_draws(4, M, d, N)
+    pmf = np.array([math.comb(N, n) for n in range(N + 1)], dtype=np.float64) / 2.0 ** N
+    for c in range(d):
+        counts = np.bincount(X[:, c], minlength=N + 1)
+        # stratum j holds u in [j/M, (j+1)/M): the count of value n is the number of strata
+        # meeting [cdf(n-1), cdf(n)), i.e. M pmf(n) rounded either way (+-1 at each edge)
+        assert np.all(np.abs(counts - M * pmf) <= 2.0)
+    keys = draws.philox_words_key(4, 1, M * d).reshape(M, d)
+    for c in range(d):
+        assert len(set(keys[:, c].tolist())) == M          # distinct keys: ranks are a permutation
+
+
+def test_stratified_marginal_is_binomial_over_seeds():
+    """Averaged over realisations, each sample is B(N, 1/2): chi^2 of the pooled draws of one
+    sample index against the pmf."""
+    import math
+    N, M = 10, 8
+    X = np.array([draws.stratified_binomial_draws(s, M, 1, N)[3, 0] for s in range(4000)])
+    pmf = np.array([math.comb(N, n) for n in range(N + 1)]) / 2.0 ** N
+    obs = np.bincount(X, minlength=N + 1)
+    exp = 4000 * pmf
+    keep = exp >= 5
+    chi2 = (((obs - exp) ** 2 / exp)[keep]).sum() + ((obs[~keep].sum() - exp[~keep].sum()) ** 2 / exp[~keep].sum())
+    assert chi2 < 30.0, chi2             # ~10 dof; 30 is p < 0.001

@@ -47,3 +47,20 @@ def test_mc_error_falls_like_one_over_t():
     curve = experiments.mse_curve(f, S_rc, Q, a, N, list(range(40)), [4, 64], s)
     m4, m64 = curve.mean(axis=0)
     assert m64 < m4 / 6.0, (m4, m64)
+
+
+def test_stratified_draws_reduce_the_mc_error():
+    """Variance reduction (reading R17): at the same T, the average MSE to the raised-cosine
+    filter is lower with stratified draws than with iid draws."""
+    H, W, d, s, N, T = 12, 12, 2, 1.0, 6, 16
+    f = random_image(H, W, d, seed=5)
+    Q, a = plan.diagonalize(np.eye(d) * 40.0 ** 2)
+    from tests.pins.test_filters import _all_outcomes_Y
+    S_rc, _, _ = native.mcsf_full(f, Q, a, N, _all_outcomes_Y(N, d), s)
+    iid, strat = [], []
+    for seed in range(30):
+        S1, _, _ = native.mcsf_full(f, Q, a, N, draws.y_draws(seed, T, d, N), s)
+        S2, _, _ = native.mcsf_full(f, Q, a, N, draws.stratified_y_draws(seed, T, d, N), s)
+        iid.append(experiments.mse(S_rc, S1))
+        strat.append(experiments.mse(S_rc, S2))
+    assert np.mean(strat) < 0.8 * np.mean(iid), (np.mean(strat), np.mean(iid))
