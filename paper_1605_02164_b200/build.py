@@ -26,15 +26,25 @@ def _sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
-def _deps_mtime():
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    files.append(os.path.join(ROOT, "include", "bfvec.h"))
-    return max(os.path.getmtime(f) for f in files)
+def _deps_mtime(src):
+    """Newest mtime of src and every local header it includes (transitively)."""
+    seen, todo = set(), [os.path.join(CSRC, src)]
+    while todo:
+        f = todo.pop()
+        if f in seen or not os.path.exists(f):
+            continue
+        seen.add(f)
+        for line in open(f, encoding="utf-8", errors="replace"):
+            line = line.strip()
+            if line.startswith("#include \""):
+                name = line.split('"')[1]
+                todo.append(os.path.normpath(os.path.join(os.path.dirname(f), name)))
+    return max(os.path.getmtime(f) for f in seen)
 
 
 def _compile(src, force):
     obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= _deps_mtime():
+    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= _deps_mtime(src):
         return obj, ""
     cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
