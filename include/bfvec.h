@@ -172,6 +172,18 @@ bf_status_t bf_vec_mse_sweep(bf_vec_plan_t plan, const float *f, const float *re
                              void *stream);
 
 /*
+ * bf_vec_srgb_to_lab / bf_vec_lab_to_srgb -- the colour transforms around Lab-space filtering
+ * ("we first performed a color transformation from the RGB to the CIE-Lab
+ * space, performed the filtering in the CIE-Lab space, and then transformed back to the RGB
+ * space"). Reading R18: sRGB transfer of IEC 61966-2-1 on values in [0, 255], RGB -> XYZ from
+ * the sRGB primaries and the D65 white, CIE 1976 L*a*b* (L* in [0, 100]). No clipping.
+ *   rgb, lab   device planar (3, npix) float32; in == out is allowed (per-pixel in place)
+ * Asynchronous on `stream`. Errors: BF_E_ARG (NULL pointer, npix < 0), BF_E_CUDA.
+ */
+bf_status_t bf_vec_srgb_to_lab(const float *rgb, float *lab, long long npix, void *stream);
+bf_status_t bf_vec_lab_to_srgb(const float *lab, float *rgb, long long npix, void *stream);
+
+/*
  * bf_vec_diag -- synchronises the plan's last stream and returns diagnostics of
  * the most recent filter/normalize call: z_min = min over pixels of Z/M and
  * n_small_z = #pixels with Z/M < z_floor (default 0.05). Returns BF_W_SMALL_Z
@@ -197,6 +209,12 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 §11). Engine 1 filters whole images only (bf_vec_filter, _host, _partial;
  *                 bf_vec_filter_rows returns BF_E_UNSUPPORTED for a proper band) and ignores
  *                 "spatial_kernel", "variant", "tile_rows" and "groups".
+ *   "colorspace"  0 (default): filter the values given; 1 (d = 3 only): f is sRGB in [0, 255]
+ *                 and bf_vec_filter / _host / _rows / bf_vec_direct convert it to CIE-Lab, filter
+ *                 in Lab (C and "value_range" in Lab units; centring mu = (50, 0, 0)) and convert
+ *                 the result back (reading R18). bf_vec_filter_partial returns
+ *                 Lab-space sums (convert after bf_vec_normalize); bf_vec_mse_sweep returns
+ *                 BF_E_UNSUPPORTED.
  *   "sampler"     frequency draws of the next bf_vec_sample_freqs / bf_vec_mse_sweep:
  *                 0 (default) iid X ~ B(N, 1/2) by popcount (reading R9); 1 stratified: per
  *                 dimension a Latin-hypercube stratification of the binomial CDF over the M
@@ -222,7 +240,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value
  *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
  *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
  *   "regs", "occupancy", "alias", "variant", "spatial_kernel", "engine", "rec_batch" (last batch
- *   size), "fir_supported" (r <= 64), "sampler", and (option "profile") "fused_ns_total",
+ *   size), "fir_supported" (r <= 64), "sampler", "colorspace", and (option "profile") "fused_ns_total",
  *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
  *   an unknown name.
  */

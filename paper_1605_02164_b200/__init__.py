@@ -9,6 +9,8 @@ from . import _lib
 
 _lib.load()
 
-from .api import BF_W_ALIAS, BF_W_SMALL_Z, BfVecError, Plan, philox4x64_10, plan_for_config  # noqa: E402
+from .api import (BF_W_ALIAS, BF_W_SMALL_Z, BfVecError, Plan, lab_to_srgb, philox4x64_10,  # noqa: E402
+                  plan_for_config, srgb_to_lab)
 
-__all__ = ["Plan", "BfVecError", "philox4x64_10", "plan_for_config", "BF_W_ALIAS", "BF_W_SMALL_Z"]
+__all__ = ["Plan", "BfVecError", "philox4x64_10", "plan_for_config", "srgb_to_lab", "lab_to_srgb",
+           "BF_W_ALIAS", "BF_W_SMALL_Z"]

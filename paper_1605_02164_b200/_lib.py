@@ -25,6 +25,8 @@ SIGNATURES = {
     "bf_vec_direct": ([_P, _P, _P, _P], _I),
     "bf_vec_diag": ([_P, _P, _P], _I),
     "bf_vec_mse_sweep": ([_P, _P, _P, _I, _P, _I, _P, _P, _P], _I),
+    "bf_vec_srgb_to_lab": ([_P, _P, ctypes.c_longlong, _P], _I),
+    "bf_vec_lab_to_srgb": ([_P, _P, ctypes.c_longlong, _P], _I),
     "bf_vec_set_option": ([_P, ctypes.c_char_p, _D], _I),
     "bf_vec_plan_info": ([_P, ctypes.c_char_p, _P], _I),
     "bf_vec_philox4x64_10": ([_P, _P, _P], _I),

@@ -186,10 +186,33 @@ class Plan:
         return float(zm.value), int(n.value)
 
 
+def _color(fn_name, x, out, stream):
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != torch.float32 or not x.is_contiguous() \
+            or x.shape[0] != 3:
+        raise ValueError("expected a contiguous float32 CUDA tensor of shape (3, ...)")
+    if out is None:
+        out = torch.empty_like(x)
+    n = x.numel() // 3
+    check(getattr(_lib.load(), fn_name)(ctypes.c_void_p(x.data_ptr()), _dev(out, tuple(x.shape), "out"), n,
+                                        _stream_ptr(stream)), fn_name)
+    return out
+
+
+def srgb_to_lab(rgb, out=None, stream=None):
+    """bf_vec_srgb_to_lab: planar (3, ...) sRGB in [0, 255] -> CIE-Lab (PAPER.md:305-308)."""
+    return _color("bf_vec_srgb_to_lab", rgb, out, stream)
+
+
+def lab_to_srgb(lab, out=None, stream=None):
+    """bf_vec_lab_to_srgb: planar (3, ...) CIE-Lab -> sRGB in [0, 255] (no clipping)."""
+    return _color("bf_vec_lab_to_srgb", lab, out, stream)
+
+
 def plan_for_config(cfg):
     """Plan for a workloads.Config (BASELINE.json configs)."""
     return Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, cfg.M, cfg.seed,
                 value_range=cfg.value_range)
 
 
-__all__ = ["Plan", "BfVecError", "philox4x64_10", "plan_for_config", "BF_W_ALIAS", "BF_W_SMALL_Z"]
+__all__ = ["Plan", "BfVecError", "philox4x64_10", "plan_for_config", "srgb_to_lab", "lab_to_srgb", "BF_W_ALIAS",
+           "BF_W_SMALL_Z"]

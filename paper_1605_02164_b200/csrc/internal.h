@@ -112,6 +112,10 @@ struct MuArg {
 cudaError_t launch_mse_accum(const float *pz, int groups, int D, int d, long long npix, const float *mu,
                              float *run, int first, const float *ref, double *out, cudaStream_t s);
 
+// sRGB <-> CIE-Lab (color.cu; reading R18), planar (3, npix), in place allowed
+cudaError_t launch_srgb_to_lab(const float *in, float *out, long long npix, cudaStream_t s);
+cudaError_t launch_lab_to_srgb(const float *in, float *out, long long npix, cudaStream_t s);
+
 // Direct filter (direct.cu)
 cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const float *w,
                           const float *A /* d x d: diag(alpha) Q^T scaled */, float *U,
@@ -139,6 +143,9 @@ struct bf_vec_plan_s {
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
     float *drec = nullptr;     // recursive engine scratch (y1, y2)
     int sampler = 0;           // 0 iid binomial draws (reading R9), 1 stratified (reading R17)
+    int lab = 0;               // 1: filter in CIE-Lab (sRGB in/out, reading R18)
+    float *dlab = nullptr;     // Lab copy of the input
+    size_t dlab_bytes = 0;
     uint64_t *dkeys = nullptr; // stratified sampler: permutation keys (M d)
     float *drun = nullptr;     // error sweep: running (P', Z) planes and per-checkpoint sums
     double *dmse = nullptr;

@@ -204,6 +204,22 @@ bf_status_t ensure_pz(bf_vec_plan_t p, size_t bytes) {
 
 void fill_mu(bf_vec_plan_t p) {
     for (int c = 0; c < 8; ++c) p->mu[c] = (c < p->d) ? (float)(0.5 * p->value_range) : 0.f;
+    if (p->lab) { p->mu[0] = 50.f; p->mu[1] = 0.f; p->mu[2] = 0.f; }   // mid L*, neutral a*, b*
+}
+
+// Lab mode: the Lab copy of `rows` rows of the caller's sRGB input (plan scratch)
+bf_status_t to_lab(bf_vec_plan_t p, const float *f, int rows, const float **out, cudaStream_t s) {
+    const size_t bytes = sizeof(float) * 3 * (size_t)rows * p->W;
+    if (p->dlab_bytes < bytes) {
+        cudaFree(p->dlab);
+        p->dlab = nullptr;
+        p->dlab_bytes = 0;
+        BF_CUDA(cudaMalloc(&p->dlab, bytes));
+        p->dlab_bytes = bytes;
+    }
+    BF_CUDA(launch_srgb_to_lab(f, p->dlab, (long long)rows * p->W, s));
+    *out = p->dlab;
+    return BF_OK;
 }
 
 // fold every pending fused-launch event interval into the running total
@@ -511,7 +527,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
         cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drun); cudaFree(p->dmse);
-        cudaFree(p->dkeys);
+        cudaFree(p->dkeys); cudaFree(p->dlab);
         for (auto &pair : p->ev)
             for (auto &e : pair)
                 if (e) cudaEventDestroy(e);
@@ -550,6 +566,10 @@ bf_status_t bf_vec_get_draws(bf_vec_plan_t p, int32_t *X, float *t, double *Q, d
 static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows, int slab_row0,
                                int row0, int row1, float *out, cudaStream_t s) {
     if (!p->sampled) return BF_E_STATE;
+    if (p->lab) {   // RGB -> CIE-Lab, filter in Lab, back to RGB
+        bf_status_t st = to_lab(p, slab, slab_rows, &slab, s);
+        if (st != BF_OK) return st;
+    }
     int groups = 1;
     int D = p->kinfo.D;
     bf_status_t st;
@@ -565,6 +585,7 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     BF_CUDA(launch_diag_reset(p->ddiag, s));
     BF_CUDA(launch_normalize_groups(p->dpz, groups, D, p->d, row1 - row0, p->W, p->mu, out,
                                     p->ddiag, 1.0f / p->M, (float)p->z_floor, s));
+    if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)(row1 - row0) * p->W, s));
     p->last_launches = (p->engine == 1) ? 2 + 2 * ((p->M + p->last_batch - 1) / p->last_batch) : 4;
     p->last = s;
     return p->alias ? BF_W_ALIAS : BF_OK;
@@ -606,6 +627,10 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k
     if (k0 == k1) {
         BF_CUDA(cudaMemsetAsync(PZ, 0, sizeof(float) * (size_t)(p->d + 1) * p->H * p->W, s));
         return BF_OK;
+    }
+    if (p->lab) {
+        bf_status_t st = to_lab(p, f, p->H, &f, s);
+        if (st != BF_OK) return st;
     }
     int groups = 1;
     bf_status_t st = (p->engine == 1) ? run_recursive(p, f, k0, k1, s, &groups)
@@ -670,7 +695,12 @@ bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *str
     for (int k = 0; k < p->d; ++k)
         for (int c = 0; c < p->d; ++c) A[k * p->d + c] = (float)(sc * p->alpha[k] * p->Q[c * p->d + k]);
     cudaStream_t s = S(stream);
+    if (p->lab) {
+        st = to_lab(p, f, p->H, &f, s);
+        if (st != BF_OK) return st;
+    }
     BF_CUDA(launch_direct(f, p->d, p->H, p->W, p->r, p->taps, A, p->dU, out, s));
+    if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)p->H * p->W, s));
     p->last_launches = 2;
     p->last = s;
     return BF_OK;
@@ -682,6 +712,7 @@ bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, 
     for (int j = 0; j < n_t; ++j)
         if (t_list[j] < 1 || t_list[j] > p->M || (j > 0 && t_list[j] <= t_list[j - 1])) return BF_E_ARG;
     if (p->device < 0 || !p->sampled) return BF_E_STATE;
+    if (p->lab) return BF_E_UNSUPPORTED;
     cudaStream_t s = S(stream);
     const long long npix = (long long)p->H * p->W;
     const size_t run_bytes = sizeof(float) * (size_t)(p->d + 1) * npix;
@@ -726,6 +757,18 @@ bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, 
     p->last_launches = 0;
     if (st == BF_OK) st = st2;
     return st;
+}
+
+bf_status_t bf_vec_srgb_to_lab(const float *rgb, float *lab, long long npix, void *stream) {
+    if (!rgb || !lab || npix < 0) return BF_E_ARG;
+    BF_CUDA(launch_srgb_to_lab(rgb, lab, npix, S(stream)));
+    return BF_OK;
+}
+
+bf_status_t bf_vec_lab_to_srgb(const float *lab, float *rgb, long long npix, void *stream) {
+    if (!rgb || !lab || npix < 0) return BF_E_ARG;
+    BF_CUDA(launch_lab_to_srgb(lab, rgb, npix, S(stream)));
+    return BF_OK;
 }
 
 bf_status_t bf_vec_diag(bf_vec_plan_t p, float *z_min, long long *n_small_z) {
@@ -776,6 +819,12 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         p->engine = (int)v;
         return BF_OK;
     }
+    if (!std::strcmp(name, "colorspace")) {
+        if ((v != 0.0 && v != 1.0) || (v == 1.0 && p->d != 3)) return BF_E_ARG;
+        p->lab = (int)v;
+        fill_mu(p);
+        return BF_OK;
+    }
     if (!std::strcmp(name, "sampler")) {
         if (v != 0.0 && v != 1.0) return BF_E_ARG;
         p->sampler = (int)v;   // takes effect at the next bf_vec_sample_freqs
@@ -812,7 +861,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"sampler", p->sampler},
+        {"spatial_kernel", p->spatial}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"sampler", p->sampler}, {"colorspace", p->lab},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)
