@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--mode", default="bands", choices=["bands", "samples"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 = library default)")
     return ap.parse_args()
 
 
@@ -212,6 +213,8 @@ def run_ours(args, cfg):
     r = cfg.radius
     plan = Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, cfg.M, cfg.seed,
                 value_range=cfg.value_range)
+    if args.variant:
+        plan.set_option("variant", args.variant)
     plan.sample_freqs()
 
     # this rank's work

@@ -4,11 +4,13 @@
 //   v4 (tensor-memory ring, mcsf_tmem.cuh):  CfgT<D, R, 16>
 #include "mcsf_fused.cuh"
 #include "mcsf_tmem.cuh"
+#include "mcsf_tmem2.cuh"
 
 namespace bfvec {
 
 #define BFV_INSTANCES(X) X(3, 2, 128, 16, 16) X(3, 4, 128, 16, 16) X(3, 6, 128, 16, 16) X(3, 10, 128, 16, 16) X(3, 15, 128, 16, 16) X(3, 24, 256, 16, 16) X(3, 30, 256, 16, 16) X(3, 48, 256, 16, 16) X(3, 64, 64, 8, 8)
 #define BFV_TMEM_INSTANCES(X) X(3, 2) X(3, 4) X(3, 6) X(3, 10) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
+#define BFV_TMEM2_INSTANCES(X) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
 
 // variant: 0 auto (v4 where compiled), 1 force v3, 2 force v4, 3 v4 with two consumer warps per pair (R = 48)
 bool fused_select_d3(int r, int variant, KernelInfo *info) {
@@ -22,6 +24,21 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
     BFV_TMEM_INSTANCES(BFV_PICKT)
 #undef BFV_PICKT
     const bool use_t = bestT != (1 << 30) && variant != 1 && (variant == 2 || bestT <= best);
+    if (variant == 4) {   // two samples per pass (mcsf_tmem2.cuh)
+        int best2 = 1 << 30;
+#define BFV_PICK2(D_, R_) \
+    if (R_ >= r && R_ < best2) best2 = R_;
+        BFV_TMEM2_INSTANCES(BFV_PICK2)
+#undef BFV_PICK2
+        if (best2 != (1 << 30)) {
+#define BFV_FILL2(D_, R_) \
+    if (R_ == best2) fill_info_tmem2<CfgT2<D_, R_>>(info);
+            BFV_TMEM2_INSTANCES(BFV_FILL2)
+#undef BFV_FILL2
+            info->variant = 4;
+            return true;
+        }
+    }
     if (variant == 3 && bestT == 48) {   // two consumer warps per pair (comparison instance)
         fill_info_tmem<CfgT<3, 48, 16, 2>>(info);
         info->variant = 3;
@@ -46,6 +63,13 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
 
 cudaError_t fused_launch_d3(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s) {
     if (info.variant == 3) return launch_tmem<CfgT<3, 48, 16, 2>>(a, grid, s);
+    if (info.variant == 4) {
+#define BFV_LAUNCH2(D_, R_) \
+    if (info.R == R_) return launch_tmem2<CfgT2<D_, R_>>(a, grid, s);
+        BFV_TMEM2_INSTANCES(BFV_LAUNCH2)
+#undef BFV_LAUNCH2
+        return cudaErrorInvalidValue;
+    }
     if (info.variant == 2) {
 #define BFV_LAUNCHT(D_, R_) \
     if (info.R == R_) return launch_tmem<CfgT<D_, R_, 16>>(a, grid, s);

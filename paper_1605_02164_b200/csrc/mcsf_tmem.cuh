@@ -18,6 +18,7 @@
 //
 // Row bookkeeping as in v3: the g-th row the producer emits in this CTA (counting
 // across samples) lives in ring slot g % HROWS and (c, s) ring slot g % RING.
+#pragma once
 #include "kernel_common.cuh"
 
 namespace bfvec {

@@ -1,0 +1,353 @@
+// mcsf_tmem2.cuh -- fused MCSF kernel v5 (variant 4): the tensor-memory row ring of v4
+// (mcsf_tmem.cuh), with TWO Monte Carlo samples per pass over a strip.
+//
+// Why: in v4 every sample re-streams the strip, re-loads f by TMA, hands every 16-row chunk
+// between the producer and consumer warp groups through one mbarrier round trip, and reads,
+// updates and writes the partial-sum tile once per sample. Pairing samples k and k+1 halves
+// all three per unit of FIR work: one TMA box of f feeds both modulations (Alg. 1),
+// one full/empty handoff covers both samples' rows, and the consumer folds both samples'
+// Re[conj(H) blur] (Eq. (18)-(19), Alg. 1) into one read-modify-write of the tile.
+//
+//  * TMEM: 512 columns = two rings of 2*HROWS columns, ring s for the pass's sample s.
+//  * producer warp w (8 warps): pair p = w & 3, sample slot s = w >> 2; sub-steps of SH = 8
+//    rows, so one warp's 8 H-pass outputs per thread cover the whole sub-step of its sample.
+//  * modulation: one f element feeds both samples' (c f, s f) pairs (2 sincos per pixel).
+//  * consumer warp p (4 warps): for each chunk, the vertical FIR of ring 0 then ring 1 with the
+//    same (looped, not duplicated) code; a pass with one sample (odd tail) skips slot 1.
+// Row bookkeeping is v4's with "sample" replaced by "pass".
+#pragma once
+#include "mcsf_tmem.cuh"
+
+namespace bfvec {
+namespace {
+
+template <int D_, int R_>
+struct CfgT2 {
+    static constexpr int D = D_;
+    static constexpr int R = R_;
+    static constexpr int KB = 16;            // output rows per chunk
+    static constexpr int SH = 8;             // rows per TMA box / sub-step
+    static constexpr int SP = 2;             // samples per pass
+    static constexpr int TX = kTX;
+    static constexpr int NP = D + 1;
+    static constexpr int NA = 256;           // producers: warp w -> pair w & 3, sample slot w >> 2
+    static constexpr int NB = 128;           // consumers: warp 8 + p -> pair p
+    static constexpr int NT = NA + NB;
+    static constexpr int CW = 1;
+    static constexpr int OR = KB;
+    static constexpr int DP = 4;
+    static constexpr int WIN = TX + 2 * R;
+    static constexpr int MS = cs_stride(WIN);
+    static constexpr int A = round_up(KB + 2 * R, 16);
+    static constexpr int HROWS = A + KB;
+    static constexpr int RING = A + KB - R;
+    static constexpr int NIN = 8 + 2 * R;
+    static constexpr int RCOLS = 2 * HROWS;                 // TMEM columns per ring
+    static constexpr int TCOLS = (SP * RCOLS <= 32) ? 32 : (SP * RCOLS <= 64) ? 64 : (SP * RCOLS <= 128) ? 128
+                               : (SP * RCOLS <= 256) ? 256 : 512;
+    static constexpr int SZ_F = SH * WIN * DP * 4;
+    static constexpr int SZ_G = NP * SH * MS * 8;           // one (buffer, slot) of G-pairs
+    static constexpr int SZ_RING = RING * TX * 8;           // one slot's (c, s) ring
+    static constexpr int OFF_F = 0;
+    static constexpr int OFF_G = round_up(OFF_F + SZ_F, 128);
+    static constexpr int OFF_RING = round_up(OFF_G + 2 * SP * SZ_G, 128);
+    static constexpr int OFF_BAR = round_up(OFF_RING + SP * SZ_RING, 128);
+    static constexpr size_t SMEM = OFF_BAR + 5 * 8 + 8;
+    static constexpr uint32_t TMA_BYTES = SZ_F;
+    static_assert(D >= 1 && D <= 3, "one TMEM lane quarter per pair");
+    static_assert(SP * RCOLS <= 512, "two rings in TMEM");
+    static_assert(SMEM <= 232448, "shared memory budget");
+    static_assert(WIN <= 256, "TMA box dimension");
+};
+
+// modulation of one SH-row sub-step for the pass's samples (np of them) into G[buf][s]
+template <class C>
+__device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0, float2 *gb1, float2 *cs0,
+                                          float2 *cs1, const float (&tk)[2][C::D], int g0, int np) {
+    constexpr int PER = (C::SH * C::WIN + C::NA - 1) / C::NA;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int it = ta + i * C::NA;
+        const int row = it / C::WIN;
+        const int j = it - row * C::WIN;
+        if (it >= C::SH * C::WIN) continue;
+        const float4 q = *reinterpret_cast<const float4 *>(fbuf + (row * C::WIN + j) * C::DP);
+        const float fv[4] = {q.x, q.y, q.z, q.w};
+        const bool inner = j >= C::R && j < C::R + C::TX;
+        const int rs = ((g0 + row) % C::RING) * C::TX + (j - C::R);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            if (s >= np) break;
+            float th = 0.f;
+#pragma unroll
+            for (int c = 0; c < C::D; ++c) th = fmaf(tk[s][c], fv[c], th);
+            float sn, cn;
+            __sincosf(th, &sn, &cn);
+            float2 *dst = (s == 0 ? gb0 : gb1) + row * C::MS + j;
+            dst[0] = make_float2(cn, sn);
+#pragma unroll
+            for (int p = 1; p < C::NP; ++p) dst[p * C::SH * C::MS] = make_float2(cn * fv[p - 1], sn * fv[p - 1]);
+            if (inner) (s == 0 ? cs0 : cs1)[rs] = make_float2(cn, sn);
+        }
+    }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_constant__ FusedArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *fbuf = reinterpret_cast<float *>(smem + C::OFF_F);
+    float2 *gbase = reinterpret_cast<float2 *>(smem + C::OFF_G);
+    float2 *csbase = reinterpret_cast<float2 *>(smem + C::OFF_RING);
+    uint64_t *tma_bar = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
+    uint64_t *full = tma_bar + 1;
+    uint64_t *empty = tma_bar + 3;
+    uint32_t *taddr_s = reinterpret_cast<uint32_t *>(tma_bar + 5);
+    constexpr int GSZ = C::NP * C::SH * C::MS;     // float2 per (buffer, slot)
+    constexpr int CSZ = C::RING * C::TX;           // float2 per slot's (c, s) ring
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int x0 = blockIdx.x * C::TX;
+    const int ty0 = a.out_row0 + blockIdx.y * a.tile_rows;
+    const int ty1 = min(ty0 + a.tile_rows, a.out_row0 + a.out_rows);
+    const int g = blockIdx.z;
+    const int ns = a.k1 - a.k0;
+    const int gk0 = a.k0 + (int)((long long)ns * g / a.groups);
+    const int gk1 = a.k0 + (int)((long long)ns * (g + 1) / a.groups);
+    const int nchunks = (ty1 - ty0 + C::KB - 1) / C::KB;
+    const int rows_per_pass = C::A + (nchunks - 1) * C::KB;   // multiple of 16
+    const int prow0 = ty0 - a.out_row0;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(taddr_s)),
+                     "n"(C::TCOLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tmap)) : "memory");
+        mbar_init(tma_bar, 1);
+        mbar_init(&full[0], C::NA);
+        mbar_init(&full[1], C::NA);
+        mbar_init(&empty[0], C::NB);
+        mbar_init(&empty[1], C::NB);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = *taddr_s;
+
+    if (gk0 < gk1) {
+        if (tid < C::NA) {
+            // ============================ PRODUCER ============================
+            const int ta = tid;
+            const int p = warp & 3;                          // pair == TMEM quarter
+            const int sw = warp >> 2;                        // sample slot of this warp's H-pass
+            const int r8 = lane & 7, cg = lane >> 3;         // item: row r8, columns 8cg .. 8cg+7
+            const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16) + (uint32_t)(sw * C::RCOLS);
+            uint32_t tparity = 0;
+            int buf = 0;
+            if (ta == 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0, C::TMA_BYTES);
+            int q = 0;
+            for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
+                const int np = min(C::SP, gk1 - k);
+                float tk[2][C::D];
+#pragma unroll
+                for (int s = 0; s < 2; ++s)
+#pragma unroll
+                    for (int c = 0; c < C::D; ++c)
+                        tk[s][c] = (c < a.d && s < np) ? __ldg(a.t + (long long)(k + s) * a.d + c) : 0.f;
+                const int gs = pass * rows_per_pass;
+                for (int ci = 0; ci < nchunks; ++ci, ++q) {
+                    const bool first_c = (ci == 0);
+                    if (first_c) {
+                        if (q >= 1) mbar_wait(&empty[(q - 1) & 1], ((q - 1) >> 1) & 1);
+                    } else if (q >= 2) {
+                        mbar_wait(&empty[q & 1], ((q - 2) >> 1) & 1);
+                    }
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const int u_begin = first_c ? 0 : C::A + (ci - 1) * C::KB;
+                    const int n_new = first_c ? C::A : C::KB;
+                    for (int s0 = 0; s0 < n_new; s0 += C::SH, buf ^= 1) {
+                        const int gsub = gs + u_begin + s0;
+                        float2 *gb0 = gbase + (2 * buf + 0) * GSZ;
+                        float2 *gb1 = gbase + (2 * buf + 1) * GSZ;
+                        mbar_wait(tma_bar, tparity);
+                        tparity ^= 1u;
+                        modulate2<C>(ta, fbuf, gb0, gb1, csbase, csbase + CSZ, tk, gsub, np);
+                        named_sync<C::NA>(1);   // G-pairs complete; fbuf free; previous H-pass done
+                        if (ta == 0) {
+                            int nu = -1;
+                            if (s0 + C::SH < n_new) nu = u_begin + s0 + C::SH;
+                            else if (ci + 1 < nchunks) nu = C::A + ci * C::KB;
+                            else if (k + C::SP < gk1) nu = 0;
+                            if (nu >= 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0 + nu, C::TMA_BYTES);
+                        }
+                        if (p < C::NP && sw < np) {
+                            // horizontal FIR: 8 outputs (row r8, columns 8cg .. 8cg+7) of sample sw
+                            const float2 *in = (sw == 0 ? gb0 : gb1) + (p * C::SH + r8) * C::MS + cg * 8;
+                            float2 acc[8];
+#pragma unroll
+                            for (int o = 0; o < 8; ++o) acc[o] = make_float2(0.f, 0.f);
+                            static_for<C::NIN / 2>([&](auto JJ) {
+                                constexpr int jj = decltype(JJ)::value;
+                                const float4 v2 = *reinterpret_cast<const float4 *>(in + 2 * jj);
+                                const float2 v[2] = {make_float2(v2.x, v2.y), make_float2(v2.z, v2.w)};
+                                static_for<2>([&](auto E) {
+                                    constexpr int e = decltype(E)::value;
+                                    constexpr int j = 2 * jj + e;
+                                    static_for<8>([&](auto O) {
+                                        constexpr int o = decltype(O)::value;
+                                        constexpr int m = j - o - C::R;
+                                        if constexpr (m >= -C::R && m <= C::R)
+                                            acc[o] = ffma2(a.w[m < 0 ? -m : m], v[e], acc[o]);
+                                    });
+                                });
+                            });
+#pragma unroll
+                            for (int s = 4; s >= 1; s >>= 1) {
+                                const bool upper = (r8 & s) != 0;
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    if ((i & s) == 0) {
+                                        const float2 send = upper ? acc[i] : acc[i + s];
+                                        float2 recv;
+                                        recv.x = __shfl_xor_sync(0xffffffffu, send.x, s);
+                                        recv.y = __shfl_xor_sync(0xffffffffu, send.y, s);
+                                        if (upper) acc[i] = recv;
+                                        else acc[i + s] = recv;
+                                    }
+                                }
+                            }
+                            const int slot = gsub % C::HROWS;   // 8 consecutive slots, no wrap
+                            tmem_st16(tq + 2 * slot, acc);
+                        }
+                        if (s0 + C::SH >= n_new) {
+                            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                            mbar_arrive(&full[q & 1]);
+                        }
+                    }
+                }
+            }
+        } else {
+            // ============================ CONSUMERS ===========================
+            const int p = warp & 3;
+            const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16);
+            const int x = x0 + lane;
+            const bool active = p < C::NP;
+            const bool xok = x < a.W;
+            const long long plane_out = (long long)a.out_rows * a.W;
+            const int plane = (p == 0) ? C::D : p - 1;
+            float *pzp = a.pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
+            constexpr int OR = C::OR;
+            constexpr int JB1 = (OR - 1 + 2 * C::R) / 16 + 1;
+            int q = 0;
+            for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
+                const int np = min(C::SP, gk1 - k);
+                const bool first_k = (k == gk0);
+                const int gs = pass * rows_per_pass;
+                for (int ci = 0; ci < nchunks; ++ci, ++q) {
+                    const int cy = ty0 + ci * C::KB;
+                    float *dst = pzp + (long long)(cy - a.out_row0) * a.W;
+                    float tot[OR];
+#pragma unroll
+                    for (int o = 0; o < OR; ++o) {
+                        const bool ok = active && xok && (cy + o < ty1);
+                        tot[o] = (!first_k && ok) ? dst[(long long)o * a.W] : 0.f;
+                    }
+                    mbar_wait(&full[q & 1], (q >> 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const int b0 = (gs + ci * C::KB) % C::HROWS;   // multiple of 16
+#pragma unroll 1
+                    for (int s = 0; s < np; ++s) {
+                        const uint32_t tr = tq + (uint32_t)(s * C::RCOLS);
+                        float2 acc[OR];
+#pragma unroll
+                        for (int o = 0; o < OR; ++o) acc[o] = make_float2(0.f, 0.f);
+                        float2 v[2][16];
+                        auto slot_of = [&](int bj) {
+                            const int slot = b0 + 16 * bj;
+                            return slot >= C::HROWS ? slot - C::HROWS : slot;
+                        };
+                        tmem_ld32(tr + 2 * slot_of(0), v[0]);
+                        tmem_wait_ld(v[0]);
+                        static_for<JB1>([&](auto B) {
+                            constexpr int bj = decltype(B)::value;
+                            if constexpr (bj + 1 < JB1) tmem_ld32(tr + 2 * slot_of(bj + 1), v[(bj + 1) & 1]);
+                            static_for<16>([&](auto JJ) {
+                                constexpr int j = 16 * bj + decltype(JJ)::value;
+                                static_for<OR>([&](auto O) {
+                                    constexpr int o = decltype(O)::value;
+                                    constexpr int m = j - o - C::R;
+                                    if constexpr (m >= -C::R && m <= C::R)
+                                        acc[o] = ffma2(a.w[m < 0 ? -m : m], v[bj & 1][decltype(JJ)::value], acc[o]);
+                                });
+                            });
+                            if constexpr (bj + 1 < JB1) tmem_wait_ld(v[(bj + 1) & 1]);
+                        });
+                        const float2 *csr = csbase + s * CSZ;
+                        int slot = (gs + ci * C::KB + C::R) % C::RING;
+#pragma unroll
+                        for (int o = 0; o < OR; ++o) {
+                            const float2 cs = csr[slot * C::TX + lane];
+                            tot[o] = fmaf(cs.x, acc[o].x, fmaf(cs.y, acc[o].y, tot[o]));
+                            slot = (slot + 1 == C::RING) ? 0 : slot + 1;
+                        }
+                    }
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    mbar_arrive(&empty[q & 1]);
+                    if (active && xok) {
+#pragma unroll
+                        for (int o = 0; o < OR; ++o)
+                            if (cy + o < ty1) dst[(long long)o * a.W] = tot[o];
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TCOLS) : "memory");
+}
+
+template <class C>
+cudaError_t launch_tmem2(const FusedArgs &a, dim3 grid, cudaStream_t s) {
+    auto k = mcsf_tmem2_kernel<C>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k<<<grid, C::NT, C::SMEM, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <class C>
+void fill_info_tmem2(KernelInfo *info) {
+    info->D = C::D;
+    info->R = C::R;
+    info->threads = C::NT;
+    info->kb = C::KB;
+    info->sh = C::SH;
+    info->dp = C::DP;
+    info->win = C::WIN;
+    info->smem = C::SMEM;
+    info->regs = 0;
+    info->occupancy = 0;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, mcsf_tmem2_kernel<C>) == cudaSuccess) info->regs = fa.numRegs;
+    if (cudaFuncSetAttribute(mcsf_tmem2_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) ==
+        cudaSuccess) {
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mcsf_tmem2_kernel<C>, C::NT, C::SMEM) == cudaSuccess)
+            info->occupancy = occ;
+    }
+    cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace bfvec
