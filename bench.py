@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 = library default)")
+    ap.add_argument("--engine", type=int, default=0, help="0 truncated FIR (default), 1 recursive O(1) engine")
+    ap.add_argument("--sigma", type=float, default=0.0, help="override the config's sigma_s (engine sweeps)")
     return ap.parse_args()
 
 
@@ -121,6 +123,35 @@ def algorithmic_flops_per_px_sample(d, r):
     FMA = 2 flops, MUL = 1 flop."""
     fma = d + 2 * 2 * (d + 1) * (2 * r + 1) + 2 * (d + 1)
     return 2 * fma + 2 * d
+
+
+def recursive_flops_per_px_sample(d):
+    """Recursive engine, FP32 work per pixel-sample independent of sigma_s:
+    modulation as above; per real plane (2(d+1)) and axis, causal + anticausal first-order
+    complex recursions over 2 poles (4 FMA-class ops each) and the output Re[A (u + v)] - g0 x
+    (2 poles x 2 directions x 2 FMA + 1); accumulate 2(d+1) FMA. FMA = 2 flops, MUL = 1."""
+    planes = 2 * (d + 1)
+    per_axis = 2 * 2 * 4 + 2 * 2 * 2 + 1
+    fma = d + planes * 2 * per_axis + 2 * (d + 1)
+    return 2 * fma + 2 * d
+
+
+KERNEL_NAMES = {1: "mcsf_fused_kernel", 2: "mcsf_tmem_kernel", 3: "mcsf_tmem_kernel(CW=2)", 4: "mcsf_tmem2_kernel"}
+
+
+def measured_traffic(cfg, kernel, units):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
+    `ncu --set full` capture of this workload (profiles/r01_traffic.json), scaled by the launch's
+    pixel-samples when the capture covered a different count; None if no capture matches."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            tab = json.load(fh)
+    except Exception:
+        return None
+    e = tab.get(f"{cfg.name}|{kernel}")
+    if not e:
+        return None
+    return (e["dram_bytes_read"] + e["dram_bytes_write"]) * units / e["units"]
 
 
 # ---------------------------------------------------------------------------
@@ -215,6 +246,8 @@ def run_ours(args, cfg):
                 value_range=cfg.value_range)
     if args.variant:
         plan.set_option("variant", args.variant)
+    if args.engine:
+        plan.set_option("engine", args.engine)
     plan.sample_freqs()
 
     # this rank's work
@@ -240,7 +273,7 @@ def run_ours(args, cfg):
         nonlocal launches_per_step
         if world == 1:
             plan.filter(f, out)
-            launches_per_step = 4           # pad, fused, diag reset, normalise
+            launches_per_step = plan.info("launches_per_filter")   # FIR: pad, fused, diag reset, normalise
         elif args.mode == "bands":
             shard.filter_bands(plan, f, s0, out=out)
             launches_per_step = 4
@@ -323,13 +356,18 @@ def run_ours(args, cfg):
     peak = fp32_peak_tflops(mhz_max)
     fused_ms = fused_ns / 1e6 / max(1, fused_calls)
     units_per_launch = rows * cfg.W * (k1 - k0)
-    flops = algorithmic_flops_per_px_sample(cfg.d, r) * units_per_launch
+    flops = (algorithmic_flops_per_px_sample(cfg.d, r) if args.engine == 0
+             else recursive_flops_per_px_sample(cfg.d)) * units_per_launch
     achieved = flops / (fused_ms / 1e3) / 1e12
+    kname = KERNEL_NAMES.get(plan.info("variant"), "mcsf_fused_kernel")
+    if args.engine == 1:
+        kname = "rec_row_kernel+rec_col_kernel"
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "mcsf_fused_kernel", "fused_ms_per_launch": fused_ms,
+            "traffic": measured_traffic(cfg, kname, units_per_launch), "kernel": kname, "fused_ms_per_launch": fused_ms,
             "peak_source": f"FP32 pipe: 148 SM x 128 lanes x 2 flop x {mhz_max} MHz (sm_max)",
             "frac_at_run_clock": (achieved / fp32_peak_tflops(clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
-            "flops_per_px_sample": algorithmic_flops_per_px_sample(cfg.d, r),
+            "flops_per_px_sample": (algorithmic_flops_per_px_sample(cfg.d, r) if args.engine == 0
+                                    else recursive_flops_per_px_sample(cfg.d)),
             "fused_share_of_step": (fused_ns / 1e6) / ms if ms > 0 else None}
 
     cpu = None
@@ -347,6 +385,7 @@ def run_ours(args, cfg):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": config_dict(cfg, world, args.mode, l2=l2_note, tile_rows=plan.info("tile_rows"),
+                                  engine=("recursive" if args.engine == 1 else "fir"),
                                   groups=plan.info("groups")),
             "mpix_per_s": cfg.H * cfg.W * args.steps / (ms_max / 1e3) / 1e6,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
@@ -361,6 +400,9 @@ def main():
     args = parse()
     from workloads import CONFIGS
     cfg = CONFIGS[args.config]
+    if args.sigma:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, sigma_s=args.sigma)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

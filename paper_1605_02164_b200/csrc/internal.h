@@ -47,7 +47,9 @@ struct KernelInfo {
     size_t smem;
     int regs;
     int occupancy;        // CTAs per SM (from the occupancy API)
-    int variant;          // 1: shared-memory ring (v3), 2: tensor-memory ring (v4)
+    int variant;          // 1: shared-memory ring (v3), 2: tensor-memory ring (v4), 3: v4 with two consumer
+                          // warps per pair, 4: v4 with two samples per pass (v5)
+    int sp = 1;           // samples per pass over a strip
 };
 
 // Kernel-set dispatch (mcsf_fused.cu). Returns false if no instance fits.

@@ -4,13 +4,15 @@
 //   v4 (tensor-memory ring, mcsf_tmem.cuh):  CfgT<D, R, 16>
 #include "mcsf_fused.cuh"
 #include "mcsf_tmem.cuh"
+#include "mcsf_tmem2.cuh"
 
 namespace bfvec {
 
 #define BFV_INSTANCES(X) X(1, 2, 64, 16, 16) X(1, 6, 64, 16, 16) X(1, 15, 64, 16, 16) X(1, 32, 64, 16, 16) X(1, 64, 64, 16, 16)
+#define BFV_TMEM2_INSTANCES(X) X(1, 15) X(1, 24) X(1, 30) X(1, 48)
 #define BFV_TMEM_INSTANCES(X) X(1, 6) X(1, 15) X(1, 24) X(1, 32) X(1, 48)
 
-// variant: 0 auto (v4 where compiled), 1 force v3, 2 force v4
+// variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 4 force v5
 bool fused_select_d1(int r, int variant, KernelInfo *info) {
     int best = 1 << 30, bestT = 1 << 30;
 #define BFV_PICK(D_, R_, NA_, KB_, SH_) \
@@ -21,6 +23,21 @@ bool fused_select_d1(int r, int variant, KernelInfo *info) {
     if (R_ >= r && R_ < bestT) bestT = R_;
     BFV_TMEM_INSTANCES(BFV_PICKT)
 #undef BFV_PICKT
+    if (variant == 4 || variant == 0) {   // two samples per pass (mcsf_tmem2.cuh), default where compiled
+        int best2 = 1 << 30;
+#define BFV_PICK2(D_, R_) \
+    if (R_ >= r && R_ < best2) best2 = R_;
+        BFV_TMEM2_INSTANCES(BFV_PICK2)
+#undef BFV_PICK2
+        if (best2 != (1 << 30) && (variant == 4 || best2 <= bestT)) {
+#define BFV_FILL2(D_, R_) \
+    if (R_ == best2) fill_info_tmem2<CfgT2<D_, R_>>(info);
+            BFV_TMEM2_INSTANCES(BFV_FILL2)
+#undef BFV_FILL2
+            info->variant = 4;
+            return true;
+        }
+    }
     const bool use_t = bestT != (1 << 30) && variant != 1 && (variant == 2 || bestT <= best);
     if (use_t) {
 #define BFV_FILLT(D_, R_) \
@@ -40,6 +57,13 @@ bool fused_select_d1(int r, int variant, KernelInfo *info) {
 }
 
 cudaError_t fused_launch_d1(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s) {
+    if (info.variant == 4) {
+#define BFV_LAUNCH2(D_, R_) \
+    if (info.R == R_) return launch_tmem2<CfgT2<D_, R_>>(a, grid, s);
+        BFV_TMEM2_INSTANCES(BFV_LAUNCH2)
+#undef BFV_LAUNCH2
+        return cudaErrorInvalidValue;
+    }
     if (info.variant == 2) {
 #define BFV_LAUNCHT(D_, R_) \
     if (info.R == R_) return launch_tmem<CfgT<D_, R_, 16>>(a, grid, s);

@@ -12,7 +12,8 @@ namespace bfvec {
 #define BFV_TMEM_INSTANCES(X) X(3, 2) X(3, 4) X(3, 6) X(3, 10) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
 #define BFV_TMEM2_INSTANCES(X) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
 
-// variant: 0 auto (v4 where compiled), 1 force v3, 2 force v4, 3 v4 with two consumer warps per pair (R = 48)
+// variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 3 v4 with two
+// consumer warps per pair (R = 48), 4 force v5 (two samples per pass)
 bool fused_select_d3(int r, int variant, KernelInfo *info) {
     int best = 1 << 30, bestT = 1 << 30;
 #define BFV_PICK(D_, R_, NA_, KB_, SH_) \
@@ -24,13 +25,13 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
     BFV_TMEM_INSTANCES(BFV_PICKT)
 #undef BFV_PICKT
     const bool use_t = bestT != (1 << 30) && variant != 1 && (variant == 2 || bestT <= best);
-    if (variant == 4) {   // two samples per pass (mcsf_tmem2.cuh)
+    if (variant == 4 || variant == 0) {   // two samples per pass (mcsf_tmem2.cuh), default where compiled
         int best2 = 1 << 30;
 #define BFV_PICK2(D_, R_) \
     if (R_ >= r && R_ < best2) best2 = R_;
         BFV_TMEM2_INSTANCES(BFV_PICK2)
 #undef BFV_PICK2
-        if (best2 != (1 << 30)) {
+        if (best2 != (1 << 30) && (variant == 4 || best2 <= bestT)) {
 #define BFV_FILL2(D_, R_) \
     if (R_ == best2) fill_info_tmem2<CfgT2<D_, R_>>(info);
             BFV_TMEM2_INSTANCES(BFV_FILL2)

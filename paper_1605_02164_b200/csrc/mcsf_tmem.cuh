@@ -370,6 +370,7 @@ cudaError_t launch_tmem(const FusedArgs &a, dim3 grid, cudaStream_t s) {
 
 template <class C>
 void fill_info_tmem(KernelInfo *info) {
+    info->sp = 1;
     info->D = C::D;
     info->R = C::R;
     info->threads = C::NT;

@@ -338,6 +338,7 @@ void fill_info_tmem2(KernelInfo *info) {
     info->smem = C::SMEM;
     info->regs = 0;
     info->occupancy = 0;
+    info->sp = C::SP;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, mcsf_tmem2_kernel<C>) == cudaSuccess) info->regs = fa.numRegs;
     if (cudaFuncSetAttribute(mcsf_tmem2_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) ==

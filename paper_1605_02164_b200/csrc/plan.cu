@@ -175,7 +175,10 @@ void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows
             // (at most 24 GiB), or 4 groups, whichever is larger
             const double pz_bytes = (double)G * (D + 1) * out_rows * (double)p->W * 4.0;
             if (G > 1 && pz_bytes > std::max(pz_budget, 4.0 * (D + 1) * out_rows * (double)p->W * 4.0)) continue;
-            const int mg = (ns + G - 1) / G;
+            // samples per group, rounded up to whole passes (v5 pairs samples: an odd group
+            // ends with a one-sample pass that costs about as much as a pair)
+            const int sp = std::max(1, ki.sp);
+            const int mg = ((ns + G - 1) / G + sp - 1) / sp * sp;
             // per sample: H rows (chunks*KB + 2R) and V rows (chunks*KB) run concurrently in
             // the two warp groups; the 2R halo rows of the first chunk are not overlapped
             const double cta = mg * (2.0 * chunks * KB + 4.0 * R + 2.0 * chunks) * row_unit + 2e-6;
@@ -586,7 +589,7 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     BF_CUDA(launch_normalize_groups(p->dpz, groups, D, p->d, row1 - row0, p->W, p->mu, out,
                                     p->ddiag, 1.0f / p->M, (float)p->z_floor, s));
     if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)(row1 - row0) * p->W, s));
-    p->last_launches = (p->engine == 1) ? 2 + 2 * ((p->M + p->last_batch - 1) / p->last_batch) : 4;
+    p->last_launches = ((p->engine == 1) ? 2 + 2 * ((p->M + p->last_batch - 1) / p->last_batch) : 4) + (p->lab ? 2 : 0);
     p->last = s;
     return p->alias ? BF_W_ALIAS : BF_OK;
 }
