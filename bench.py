@@ -139,17 +139,18 @@ def recursive_flops_per_px_sample(d):
 KERNEL_NAMES = {1: "mcsf_fused_kernel", 2: "mcsf_tmem_kernel", 3: "mcsf_tmem_kernel(CW=2)", 4: "mcsf_tmem2_kernel"}
 
 
-def measured_traffic(cfg, kernel, units):
+def measured_traffic(cfg, kernel, units, schedule):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the committed
-    `ncu --set full` capture of this workload (profiles/r01_traffic.json), scaled by the launch's
-    pixel-samples when the capture covered a different count; None if no capture matches."""
+    `ncu --set full` capture of this workload and launch schedule (profiles/r01_traffic.json),
+    scaled by the launch's pixel-samples; None if no capture matches (the partial-sum traffic
+    depends on the (tile_rows, groups) schedule)."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
             tab = json.load(fh)
     except Exception:
         return None
     e = tab.get(f"{cfg.name}|{kernel}")
-    if not e:
+    if not e or e.get("schedule") != schedule:
         return None
     return (e["dram_bytes_read"] + e["dram_bytes_write"]) * units / e["units"]
 
@@ -363,7 +364,9 @@ def run_ours(args, cfg):
     if args.engine == 1:
         kname = "rec_row_kernel+rec_col_kernel"
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": measured_traffic(cfg, kname, units_per_launch), "kernel": kname, "fused_ms_per_launch": fused_ms,
+            "traffic": measured_traffic(cfg, kname, units_per_launch,
+                                        {"tile_rows": plan.info("tile_rows"), "groups": plan.info("groups")}),
+            "kernel": kname, "fused_ms_per_launch": fused_ms,
             "peak_source": f"FP32 pipe: 148 SM x 128 lanes x 2 flop x {mhz_max} MHz (sm_max)",
             "frac_at_run_clock": (achieved / fp32_peak_tflops(clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
             "flops_per_px_sample": (algorithmic_flops_per_px_sample(cfg.d, r) if args.engine == 0
