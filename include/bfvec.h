@@ -197,10 +197,14 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *   "value_range" nominal data range R used for the alias warning (default 255)
  *   "tile_rows"   force the row-tile height of the fused kernel (0 = auto)
  *   "groups"      force the number of sample groups (0 = auto)
- *   "variant"     fused-kernel variant: 0 auto, 1 shared-memory ring, 2 tensor-memory
- *                 ring (d <= 3 only), 3 tensor-memory ring with two consumer warps per
- *                 (cos, sin) pair (d <= 3, r in (30, 48]); BF_E_UNSUPPORTED if not compiled
- *                 for the plan
+ *   "variant"     fused-kernel variant: 0 auto (4 where compiled, else 2, else 1),
+ *                 1 shared-memory ring (v3), 2 tensor-memory ring (v4, d <= 3), 3 v4 with two
+ *                 consumer warps per (cos, sin) pair (d <= 3, r in (30, 48]), 4 v5: tensor-
+ *                 memory double ring, two samples per pass, two consumer warps per pair
+ *                 (d <= 3, r in (10, 48]), 5 v5 with one consumer warp per pair (d = 3,
+ *                 r in (30, 48]), 6 v3 with one H-pass item per producer thread (d in 5..8,
+ *                 r in (15, 24]); a variant not compiled for the plan falls back to the default
+ *                 order
  *   "engine"      how Alg. 1 step 10 convolves: 0 (default) the truncated
  *                 separable window [-r, r] of Eq. (1) / "spatial_kernel", O(r) per pixel-sample
  *                 (fused sm_100a kernel); 1 the recursive O(1)-in-sigma_s engine of PAPER.md:204

@@ -13,7 +13,8 @@ namespace bfvec {
 #define BFV_TMEM2_INSTANCES(X) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
 
 // variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 3 v4 with two
-// consumer warps per pair (R = 48), 4 force v5 (two samples per pass)
+// consumer warps per pair (R = 48), 4 force v5 (two samples per pass, two consumer
+// warps per pair), 5 v5 with one consumer warp per pair (R = 48)
 bool fused_select_d3(int r, int variant, KernelInfo *info) {
     int best = 1 << 30, bestT = 1 << 30;
 #define BFV_PICK(D_, R_, NA_, KB_, SH_) \
@@ -33,12 +34,17 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
 #undef BFV_PICK2
         if (best2 != (1 << 30) && (variant == 4 || best2 <= bestT)) {
 #define BFV_FILL2(D_, R_) \
-    if (R_ == best2) fill_info_tmem2<CfgT2<D_, R_>>(info);
+    if (R_ == best2) fill_info_tmem2<CfgT2<D_, R_, 2>>(info);
             BFV_TMEM2_INSTANCES(BFV_FILL2)
 #undef BFV_FILL2
             info->variant = 4;
             return true;
         }
+    }
+    if (variant == 5 && bestT == 48) {   // v5 with one consumer warp per pair (comparison instance)
+        fill_info_tmem2<CfgT2<3, 48, 1>>(info);
+        info->variant = 5;
+        return true;
     }
     if (variant == 3 && bestT == 48) {   // two consumer warps per pair (comparison instance)
         fill_info_tmem<CfgT<3, 48, 16, 2>>(info);
@@ -64,9 +70,10 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
 
 cudaError_t fused_launch_d3(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s) {
     if (info.variant == 3) return launch_tmem<CfgT<3, 48, 16, 2>>(a, grid, s);
+    if (info.variant == 5) return launch_tmem2<CfgT2<3, 48, 1>>(a, grid, s);
     if (info.variant == 4) {
 #define BFV_LAUNCH2(D_, R_) \
-    if (info.R == R_) return launch_tmem2<CfgT2<D_, R_>>(a, grid, s);
+    if (info.R == R_) return launch_tmem2<CfgT2<D_, R_, 2>>(a, grid, s);
         BFV_TMEM2_INSTANCES(BFV_LAUNCH2)
 #undef BFV_LAUNCH2
         return cudaErrorInvalidValue;

@@ -21,7 +21,7 @@
 namespace bfvec {
 namespace {
 
-template <int D_, int R_>
+template <int D_, int R_, int CW_ = 1>
 struct CfgT2 {
     static constexpr int D = D_;
     static constexpr int R = R_;
@@ -31,10 +31,10 @@ struct CfgT2 {
     static constexpr int TX = kTX;
     static constexpr int NP = D + 1;
     static constexpr int NA = 256;           // producers: warp w -> pair w & 3, sample slot w >> 2
-    static constexpr int NB = 128;           // consumers: warp 8 + p -> pair p
+    static constexpr int CW = CW_;           // consumer warps per pair: warp 8 + w -> pair w & 3,
+    static constexpr int OR = KB / CW_;      //   output rows OR (w >> 2) .. + OR of every chunk
+    static constexpr int NB = 128 * CW_;
     static constexpr int NT = NA + NB;
-    static constexpr int CW = 1;
-    static constexpr int OR = KB;
     static constexpr int DP = 4;
     static constexpr int WIN = TX + 2 * R;
     static constexpr int MS = cs_stride(WIN);
@@ -55,10 +55,33 @@ struct CfgT2 {
     static constexpr size_t SMEM = OFF_BAR + 5 * 8 + 8;
     static constexpr uint32_t TMA_BYTES = SZ_F;
     static_assert(D >= 1 && D <= 3, "one TMEM lane quarter per pair");
+    static_assert(CW_ == 1 || CW_ == 2, "one or two consumer warps per pair");
     static_assert(SP * RCOLS <= 512, "two rings in TMEM");
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(WIN <= 256, "TMA box dimension");
 };
+
+// TMEM load of LR ring rows (2 LR columns) into LR float2, and the matching wait
+__device__ __forceinline__ void tmem_ld16c(uint32_t taddr, float2 (&v)[8]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[1].x), "=f"(v[1].y), "=f"(v[2].x), "=f"(v[2].y), "=f"(v[3].x),
+          "=f"(v[3].y), "=f"(v[4].x), "=f"(v[4].y), "=f"(v[5].x), "=f"(v[5].y), "=f"(v[6].x), "=f"(v[6].y),
+          "=f"(v[7].x), "=f"(v[7].y)
+        : "r"(taddr)
+        : "memory");
+}
+template <int LR>
+__device__ __forceinline__ void tmem_ld_rows(uint32_t taddr, float2 (&v)[LR]) {
+    if constexpr (LR == 16) tmem_ld32(taddr, v);
+    else tmem_ld16c(taddr, v);
+}
+template <int LR>
+__device__ __forceinline__ void tmem_wait_rows(float2 (&v)[LR]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < LR; ++i) asm volatile("" : "+f"(v[i].x), "+f"(v[i].y));
+}
 
 // modulation of one SH-row sub-step for the pass's samples (np of them) into G[buf][s]
 template <class C>
@@ -232,7 +255,12 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
             }
         } else {
             // ============================ CONSUMERS ===========================
+            // warp 8 + w: pair p = w & 3 (TMEM quarter p); part h = w >> 2 owns output rows
+            // h*OR .. h*OR + OR - 1 of every chunk. Both parts run the same code: the window of
+            // part h starts h*OR ring rows later (8-row TMEM loads when OR = 8).
             const int p = warp & 3;
+            const int h = (warp - C::NA / 32) >> 2;
+            const int H0 = h * C::OR;
             const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16);
             const int x = x0 + lane;
             const bool active = p < C::NP;
@@ -241,14 +269,15 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
             const int plane = (p == 0) ? C::D : p - 1;
             float *pzp = a.pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
             constexpr int OR = C::OR;
-            constexpr int JB1 = (OR - 1 + 2 * C::R) / 16 + 1;
+            constexpr int LR = (OR == 16) ? 16 : 8;                  // ring rows per TMEM load
+            constexpr int JB1 = (OR - 1 + 2 * C::R) / LR + 1;        // loads per window
             int q = 0;
             for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
                 const int np = min(C::SP, gk1 - k);
                 const bool first_k = (k == gk0);
                 const int gs = pass * rows_per_pass;
                 for (int ci = 0; ci < nchunks; ++ci, ++q) {
-                    const int cy = ty0 + ci * C::KB;
+                    const int cy = ty0 + ci * C::KB + H0;
                     float *dst = pzp + (long long)(cy - a.out_row0) * a.W;
                     float tot[OR];
 #pragma unroll
@@ -258,25 +287,25 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                     }
                     mbar_wait(&full[q & 1], (q >> 1) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const int b0 = (gs + ci * C::KB) % C::HROWS;   // multiple of 16
+                    const int b0 = (gs + ci * C::KB + H0) % C::HROWS;   // multiple of LR
 #pragma unroll 1
                     for (int s = 0; s < np; ++s) {
                         const uint32_t tr = tq + (uint32_t)(s * C::RCOLS);
                         float2 acc[OR];
 #pragma unroll
                         for (int o = 0; o < OR; ++o) acc[o] = make_float2(0.f, 0.f);
-                        float2 v[2][16];
+                        float2 v[2][LR];
                         auto slot_of = [&](int bj) {
-                            const int slot = b0 + 16 * bj;
+                            const int slot = b0 + LR * bj;
                             return slot >= C::HROWS ? slot - C::HROWS : slot;
                         };
-                        tmem_ld32(tr + 2 * slot_of(0), v[0]);
-                        tmem_wait_ld(v[0]);
+                        tmem_ld_rows<LR>(tr + 2 * slot_of(0), v[0]);
+                        tmem_wait_rows<LR>(v[0]);
                         static_for<JB1>([&](auto B) {
                             constexpr int bj = decltype(B)::value;
-                            if constexpr (bj + 1 < JB1) tmem_ld32(tr + 2 * slot_of(bj + 1), v[(bj + 1) & 1]);
-                            static_for<16>([&](auto JJ) {
-                                constexpr int j = 16 * bj + decltype(JJ)::value;
+                            if constexpr (bj + 1 < JB1) tmem_ld_rows<LR>(tr + 2 * slot_of(bj + 1), v[(bj + 1) & 1]);
+                            static_for<LR>([&](auto JJ) {
+                                constexpr int j = LR * bj + decltype(JJ)::value;
                                 static_for<OR>([&](auto O) {
                                     constexpr int o = decltype(O)::value;
                                     constexpr int m = j - o - C::R;
@@ -284,10 +313,10 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                                         acc[o] = ffma2(a.w[m < 0 ? -m : m], v[bj & 1][decltype(JJ)::value], acc[o]);
                                 });
                             });
-                            if constexpr (bj + 1 < JB1) tmem_wait_ld(v[(bj + 1) & 1]);
+                            if constexpr (bj + 1 < JB1) tmem_wait_rows<LR>(v[(bj + 1) & 1]);
                         });
                         const float2 *csr = csbase + s * CSZ;
-                        int slot = (gs + ci * C::KB + C::R) % C::RING;
+                        int slot = (gs + ci * C::KB + H0 + C::R) % C::RING;
 #pragma unroll
                         for (int o = 0; o < OR; ++o) {
                             const float2 cs = csr[slot * C::TX + lane];
