@@ -288,6 +288,12 @@ def run_ours(args, cfg):
     if in_bytes <= 256e6:
         flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device=dev)
 
+    # untimed pre-warm until ~0.3 s of work has run: the SM clock ramps up from idle over a few
+    # milliseconds, longer than W steps of the small configs take (then the W warm-up steps)
+    t_warm = time.perf_counter()
+    while time.perf_counter() - t_warm < 0.3:
+        step()
+        torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()

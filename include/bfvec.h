@@ -202,9 +202,8 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 consumer warps per (cos, sin) pair (d <= 3, r in (30, 48]), 4 v5: tensor-
  *                 memory double ring, two samples per pass, two consumer warps per pair
  *                 (d <= 3, r in (10, 48]), 5 v5 with one consumer warp per pair (d = 3,
- *                 r in (30, 48]), 6 v3 with one H-pass item per producer thread (d in 5..8,
- *                 r in (15, 24]); a variant not compiled for the plan falls back to the default
- *                 order
+ *                 r in (30, 48]); a variant not compiled for the plan falls back to the
+ *                 default order
  *   "engine"      how Alg. 1 step 10 convolves: 0 (default) the truncated
  *                 separable window [-r, r] of Eq. (1) / "spatial_kernel", O(r) per pixel-sample
  *                 (fused sm_100a kernel); 1 the recursive O(1)-in-sigma_s engine of PAPER.md:204

@@ -90,6 +90,11 @@ EDGE = [
     (50, 50, 3, 0.7, 10, 1, 8, "full"),       # M = 1, r = 3 (padded radius)
     (131, 77, 3, 5.0, 30, 17, 9, "full"),     # several tiles and a ragged tail
     (70, 40, 4, 3.3, 20, 10, 10, "diag"),     # d = 4, r = 10 (padded radius)
+    (150, 90, 3, 21.3, 40, 5, 11, "diag"),    # r = 64: the largest FIR radius (v3 instance)
+    (96, 70, 8, 8.0, 30, 4, 12, "full"),      # d = 8 at config 4's r = 24
+    (90, 64, 4, 16.0, 40, 3, 13, "diag"),     # d = 4, r = 48 (v3)
+    (64, 64, 3, 16.0, 40, 3, 14, "full"),     # r = 48 default kernel (v5): one sample pair + a one-sample tail
+    (64, 64, 3, 10.0, 40, 2, 15, "full"),     # v5 at r = 30 with a single pass
 ]
 
 
