@@ -225,7 +225,8 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 reading R17; the paper's "improving the Monte Carlo integration",
  *                 PAPER.md:313). Same estimator Eq. (14); X still B(N, 1/2)-distributed.
  *   "rec_batch"   engine 1: samples per batch (0 = auto from free device memory; each sample
- *                 in flight holds 5 (d+1) fp32 planes of H x W scratch)
+ *                 in flight holds 5 (d+1) fp32 planes of H x W scratch; at most 256 and 40 % of
+ *                 the free device memory)
  *   "spatial_kernel" separable spatial taps on the window [-r, r], r = ceil(3 sigma_s):
  *                 0 Gaussian of Eq. (1) (default), 1 box w(m) = 1, 2 hat w(m) = r + 1 - |m|
  *                 ("any arbitrary spatial filter (such as a box or hat filter)";

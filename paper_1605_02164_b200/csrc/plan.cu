@@ -413,7 +413,7 @@ bf_status_t run_recursive(bf_vec_plan_t p, const float *f, int k0, int k1, cudaS
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
     cudaGetLastError();
-    int nb = (int)std::max(1.0, std::min<double>(16.0, 0.4 * (free_b + p->drec_bytes + p->pz_bytes) / per));
+    int nb = (int)std::max(1.0, std::min<double>(256.0, 0.4 * (free_b + p->drec_bytes + p->pz_bytes) / per));
     if (p->force_batch > 0) nb = p->force_batch;
     nb = std::min(nb, ns);
     bf_status_t st = ensure_rec_scratch(p, nb);
