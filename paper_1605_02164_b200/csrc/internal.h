@@ -155,6 +155,7 @@ struct bf_vec_plan_s {
     int dmse_n = 0;
     size_t drec_bytes = 0;
     int last_batch = 0;
+    size_t free_mem = 0;       // free device memory at the first launch (0 = not queried yet)
     // device state (lazily created)
     int device = -1;
     bool sampled = false;

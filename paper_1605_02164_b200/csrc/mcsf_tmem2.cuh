@@ -51,7 +51,9 @@ struct CfgT2 {
     static constexpr int OFF_F = 0;
     static constexpr int OFF_G = round_up(OFF_F + SZ_F, 128);
     static constexpr int OFF_RING = round_up(OFF_G + 2 * SP * SZ_G, 128);
-    static constexpr int OFF_BAR = round_up(OFF_RING + SP * SZ_RING, 128);
+    static constexpr int SZ_TP = (NA / 32) * TX * 9 * 8;      // per producer warp: 32 columns x 9 float2
+    static constexpr int OFF_TP = round_up(OFF_RING + SP * SZ_RING, 128);
+    static constexpr int OFF_BAR = round_up(OFF_TP + SZ_TP, 128);
     static constexpr size_t SMEM = OFF_BAR + 5 * 8 + 8;
     static constexpr uint32_t TMA_BYTES = SZ_F;
     static_assert(D >= 1 && D <= 3, "one TMEM lane quarter per pair");
@@ -109,7 +111,8 @@ __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0
             float2 *dst = (s == 0 ? gb0 : gb1) + row * C::MS + j;
             dst[0] = make_float2(cn, sn);
 #pragma unroll
-            for (int p = 1; p < C::NP; ++p) dst[p * C::SH * C::MS] = make_float2(cn * fv[p - 1], sn * fv[p - 1]);
+            for (int p = 1; p < C::NP; ++p)
+                dst[p * C::SH * C::MS] = __fmul2_rn(make_float2(cn, sn), make_float2(fv[p - 1], fv[p - 1]));
             if (inner) (s == 0 ? cs0 : cs1)[rs] = make_float2(cn, sn);
         }
     }
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
     float *fbuf = reinterpret_cast<float *>(smem + C::OFF_F);
     float2 *gbase = reinterpret_cast<float2 *>(smem + C::OFF_G);
     float2 *csbase = reinterpret_cast<float2 *>(smem + C::OFF_RING);
+    float2 *tpose = reinterpret_cast<float2 *>(smem + C::OFF_TP);
     uint64_t *tma_bar = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
     uint64_t *full = tma_bar + 1;
     uint64_t *empty = tma_bar + 3;
@@ -227,21 +231,16 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                                     });
                                 });
                             });
+                            // transpose through this warp's shared-memory tile: lane (r8, cg) holds
+                            // row r8 of columns 8cg..8cg+7; lane x needs rows 0..7 of column x.
+                            // Stride 9 float2 per column: both directions are bank-conflict free.
+                            float2 *tt = tpose + warp * (C::TX * 9);
 #pragma unroll
-                            for (int s = 4; s >= 1; s >>= 1) {
-                                const bool upper = (r8 & s) != 0;
+                            for (int o = 0; o < 8; ++o) tt[(8 * cg + o) * 9 + r8] = acc[o];
+                            __syncwarp();
 #pragma unroll
-                                for (int i = 0; i < 8; ++i) {
-                                    if ((i & s) == 0) {
-                                        const float2 send = upper ? acc[i] : acc[i + s];
-                                        float2 recv;
-                                        recv.x = __shfl_xor_sync(0xffffffffu, send.x, s);
-                                        recv.y = __shfl_xor_sync(0xffffffffu, send.y, s);
-                                        if (upper) acc[i] = recv;
-                                        else acc[i + s] = recv;
-                                    }
-                                }
-                            }
+                            for (int o = 0; o < 8; ++o) acc[o] = tt[lane * 9 + o];
+                            __syncwarp();
                             const int slot = gsub % C::HROWS;   // 8 consecutive slots, no wrap
                             tmem_st16(tq + 2 * slot, acc);
                         }
