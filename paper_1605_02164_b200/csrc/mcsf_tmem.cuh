@@ -54,7 +54,9 @@ struct CfgT {
     static constexpr int OFF_F = 0;
     static constexpr int OFF_G = round_up(OFF_F + SZ_F, 128);
     static constexpr int OFF_RING = round_up(OFF_G + 2 * SZ_G, 128);
-    static constexpr int OFF_BAR = round_up(OFF_RING + SZ_RING, 128);
+    static constexpr int SZ_TP = (NA / 32) * TX * 9 * 8;      // per producer warp: 32 columns x 9 float2
+    static constexpr int OFF_TP = round_up(OFF_RING + SZ_RING, 128);
+    static constexpr int OFF_BAR = round_up(OFF_TP + SZ_TP, 128);
     static constexpr size_t SMEM = OFF_BAR + 5 * 8 + 8;  // tma, full[2], empty[2], tmem address
     static constexpr uint32_t TMA_BYTES = SZ_F;
     static constexpr int MINB = 1;
@@ -118,7 +120,8 @@ __device__ __forceinline__ void modulate_g(int ta, const float *fbuf, float2 *gb
         float2 *dst = gbuf + row * C::MS + j;
         dst[0] = cs;                                              // Z pair: (c, s)
 #pragma unroll
-        for (int p = 1; p < C::NP; ++p) dst[p * C::SH * C::MS] = make_float2(c * fv[p - 1], s * fv[p - 1]);
+        for (int p = 1; p < C::NP; ++p)
+            dst[p * C::SH * C::MS] = __fmul2_rn(make_float2(c, s), make_float2(fv[p - 1], fv[p - 1]));
         if (j >= C::R && j < C::R + C::TX) csring[((g0 + row) % C::RING) * C::TX + (j - C::R)] = cs;
     }
 }
@@ -129,6 +132,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem_kernel(const __grid_consta
     float *fbuf = reinterpret_cast<float *>(smem + C::OFF_F);
     float2 *gbuf = reinterpret_cast<float2 *>(smem + C::OFF_G);
     float2 *csring = reinterpret_cast<float2 *>(smem + C::OFF_RING);
+    float2 *tpose = reinterpret_cast<float2 *>(smem + C::OFF_TP);
     uint64_t *tma_bar = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
     uint64_t *full = tma_bar + 1;
     uint64_t *empty = tma_bar + 3;
@@ -229,23 +233,16 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem_kernel(const __grid_consta
                                     });
                                 });
                             });
-                            // 8x8 transpose inside each group of 8 lanes (same cg): lane 8cg + o ends
-                            // with rows 0..7 of column 8cg + o
+                            // transpose through this warp's shared-memory tile: lane (r8, cg) holds
+                            // row r8 of columns 8cg..8cg+7; lane x needs rows 0..7 of column x
+                            // (stride 9 float2 per column: conflict-free both ways)
+                            float2 *tt = tpose + warp * (C::TX * 9);
 #pragma unroll
-                            for (int s = 4; s >= 1; s >>= 1) {
-                                const bool upper = (r8 & s) != 0;
+                            for (int o = 0; o < 8; ++o) tt[(8 * cg + o) * 9 + r8] = acc[o];
+                            __syncwarp();
 #pragma unroll
-                                for (int i = 0; i < 8; ++i) {
-                                    if ((i & s) == 0) {
-                                        const float2 send = upper ? acc[i] : acc[i + s];
-                                        float2 recv;
-                                        recv.x = __shfl_xor_sync(0xffffffffu, send.x, s);
-                                        recv.y = __shfl_xor_sync(0xffffffffu, send.y, s);
-                                        if (upper) acc[i] = recv;
-                                        else acc[i + s] = recv;
-                                    }
-                                }
-                            }
+                            for (int o = 0; o < 8; ++o) acc[o] = tt[lane * 9 + o];
+                            __syncwarp();
                             const int slot = (gsub + 8 * rh) % C::HROWS;   // 8 consecutive slots, no wrap
                             tmem_st16(tq + 2 * slot, acc);
                         }
