@@ -199,10 +199,11 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *   "groups"      force the number of sample groups (0 = auto)
  *   "variant"     fused-kernel variant: 0 auto (4 where compiled, else 2, else 1),
  *                 1 shared-memory ring (v3), 2 tensor-memory ring (v4, d <= 3), 3 v4 with two
- *                 consumer warps per (cos, sin) pair (d <= 3, r in (30, 48]), 4 v5: tensor-
- *                 memory double ring, two samples per pass, two consumer warps per pair
- *                 (d <= 3, r in (10, 48]), 5 v5 with one consumer warp per pair (d = 3,
- *                 r in (30, 48]); a variant not compiled for the plan falls back to the
+ *                 consumer warps per (cos, sin) pair (d <= 3, r in (30, 48]), 4 v6: tensor-
+ *                 memory double ring, two samples per pass, two consumer warps per pair,
+ *                 four dedicated modulation warps (d <= 3, r in (10, 48]), 5 v5 with one
+ *                 consumer warp per pair, 6 v5c (v6 without the modulation warps) (both
+ *                 d = 3, r in (30, 48]); a variant not compiled for the plan falls back to the
  *                 default order
  *   "engine"      how Alg. 1 step 10 convolves: 0 (default) the truncated
  *                 separable window [-r, r] of Eq. (1) / "spatial_kernel", O(r) per pixel-sample

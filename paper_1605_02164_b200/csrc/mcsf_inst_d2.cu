@@ -31,7 +31,7 @@ bool fused_select_d2(int r, int variant, KernelInfo *info) {
 #undef BFV_PICK2
         if (best2 != (1 << 30) && (variant == 4 || best2 <= bestT)) {
 #define BFV_FILL2(D_, R_) \
-    if (R_ == best2) fill_info_tmem2<CfgT2<D_, R_, 2>>(info);
+    if (R_ == best2) fill_info_tmem2<CfgT2<D_, R_, 2, 4>>(info);
             BFV_TMEM2_INSTANCES(BFV_FILL2)
 #undef BFV_FILL2
             info->variant = 4;
@@ -59,7 +59,7 @@ bool fused_select_d2(int r, int variant, KernelInfo *info) {
 cudaError_t fused_launch_d2(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s) {
     if (info.variant == 4) {
 #define BFV_LAUNCH2(D_, R_) \
-    if (info.R == R_) return launch_tmem2<CfgT2<D_, R_, 2>>(a, grid, s);
+    if (info.R == R_) return launch_tmem2<CfgT2<D_, R_, 2, 4>>(a, grid, s);
         BFV_TMEM2_INSTANCES(BFV_LAUNCH2)
 #undef BFV_LAUNCH2
         return cudaErrorInvalidValue;

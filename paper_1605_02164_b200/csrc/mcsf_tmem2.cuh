@@ -21,7 +21,7 @@
 namespace bfvec {
 namespace {
 
-template <int D_, int R_, int CW_ = 1>
+template <int D_, int R_, int CW_ = 1, int MW_ = 0>
 struct CfgT2 {
     static constexpr int D = D_;
     static constexpr int R = R_;
@@ -34,13 +34,15 @@ struct CfgT2 {
     static constexpr int CW = CW_;           // consumer warps per pair: warp 8 + w -> pair w & 3,
     static constexpr int OR = KB / CW_;      //   output rows OR (w >> 2) .. + OR of every chunk
     static constexpr int NB = 128 * CW_;
-    static constexpr int NT = NA + NB;
+    static constexpr int MW = MW_;           // dedicated modulation warps (0: the producers modulate)
+    static constexpr int NM = 32 * MW_;
+    static constexpr int NT = NA + NB + NM;
     static constexpr int DP = 4;
     static constexpr int WIN = TX + 2 * R;
     static constexpr int MS = cs_stride(WIN);
     static constexpr int A = round_up(KB + 2 * R, 16);
     static constexpr int HROWS = A + KB;
-    static constexpr int RING = A + KB - R;
+    static constexpr int RING = A + KB - R + (MW_ > 0 ? 2 * SH : 0);   // modulators run <= 2 sub-steps ahead
     static constexpr int NIN = 8 + 2 * R;
     static constexpr int RCOLS = 2 * HROWS;                 // TMEM columns per ring
     static constexpr int TCOLS = (SP * RCOLS <= 32) ? 32 : (SP * RCOLS <= 64) ? 64 : (SP * RCOLS <= 128) ? 128
@@ -54,10 +56,11 @@ struct CfgT2 {
     static constexpr int SZ_TP = (NA / 32) * TX * 9 * 8;      // per producer warp: 32 columns x 9 float2
     static constexpr int OFF_TP = round_up(OFF_RING + SP * SZ_RING, 128);
     static constexpr int OFF_BAR = round_up(OFF_TP + SZ_TP, 128);
-    static constexpr size_t SMEM = OFF_BAR + 5 * 8 + 8;
+    static constexpr size_t SMEM = OFF_BAR + 9 * 8 + 8;    // tma, full[2], empty[2], gfull[2], gempty[2]
     static constexpr uint32_t TMA_BYTES = SZ_F;
     static_assert(D >= 1 && D <= 3, "one TMEM lane quarter per pair");
     static_assert(CW_ == 1 || CW_ == 2, "one or two consumer warps per pair");
+    static_assert(MW_ == 0 || MW_ == 4, "no or four modulation warps");
     static_assert(SP * RCOLS <= 512, "two rings in TMEM");
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(WIN <= 256, "TMA box dimension");
@@ -86,13 +89,13 @@ __device__ __forceinline__ void tmem_wait_rows(float2 (&v)[LR]) {
 }
 
 // modulation of one SH-row sub-step for the pass's samples (np of them) into G[buf][s]
-template <class C>
+template <class C, int NTH>
 __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0, float2 *gb1, float2 *cs0,
                                           float2 *cs1, const float (&tk)[2][C::D], int g0, int np) {
-    constexpr int PER = (C::SH * C::WIN + C::NA - 1) / C::NA;
+    constexpr int PER = (C::SH * C::WIN + NTH - 1) / NTH;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
-        const int it = ta + i * C::NA;
+        const int it = ta + i * NTH;
         const int row = it / C::WIN;
         const int j = it - row * C::WIN;
         if (it >= C::SH * C::WIN) continue;
@@ -128,7 +131,9 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
     uint64_t *tma_bar = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
     uint64_t *full = tma_bar + 1;
     uint64_t *empty = tma_bar + 3;
-    uint32_t *taddr_s = reinterpret_cast<uint32_t *>(tma_bar + 5);
+    uint64_t *gfull = tma_bar + 5;    // modulators -> H-pass producers, per G buffer
+    uint64_t *gempty = tma_bar + 7;   // H-pass producers -> modulators
+    uint32_t *taddr_s = reinterpret_cast<uint32_t *>(tma_bar + 9);
     constexpr int GSZ = C::NP * C::SH * C::MS;     // float2 per (buffer, slot)
     constexpr int CSZ = C::RING * C::TX;           // float2 per slot's (c, s) ring
 
@@ -158,6 +163,10 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
         mbar_init(&full[1], C::NA);
         mbar_init(&empty[0], C::NB);
         mbar_init(&empty[1], C::NB);
+        mbar_init(&gfull[0], C::NM > 0 ? C::NM : 1);
+        mbar_init(&gfull[1], C::NM > 0 ? C::NM : 1);
+        mbar_init(&gempty[0], C::NA);
+        mbar_init(&gempty[1], C::NA);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -173,8 +182,8 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
             const int r8 = lane & 7, cg = lane >> 3;         // item: row r8, columns 8cg .. 8cg+7
             const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16) + (uint32_t)(sw * C::RCOLS);
             uint32_t tparity = 0;
-            int buf = 0;
-            if (ta == 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0, C::TMA_BYTES);
+            int buf = 0, it = 0;
+            if (C::MW == 0 && ta == 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0, C::TMA_BYTES);
             int q = 0;
             for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
                 const int np = min(C::SP, gk1 - k);
@@ -195,20 +204,24 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const int u_begin = first_c ? 0 : C::A + (ci - 1) * C::KB;
                     const int n_new = first_c ? C::A : C::KB;
-                    for (int s0 = 0; s0 < n_new; s0 += C::SH, buf ^= 1) {
+                    for (int s0 = 0; s0 < n_new; s0 += C::SH, buf ^= 1, ++it) {
                         const int gsub = gs + u_begin + s0;
                         float2 *gb0 = gbase + (2 * buf + 0) * GSZ;
                         float2 *gb1 = gbase + (2 * buf + 1) * GSZ;
-                        mbar_wait(tma_bar, tparity);
-                        tparity ^= 1u;
-                        modulate2<C>(ta, fbuf, gb0, gb1, csbase, csbase + CSZ, tk, gsub, np);
-                        named_sync<C::NA>(1);   // G-pairs complete; fbuf free; previous H-pass done
-                        if (ta == 0) {
-                            int nu = -1;
-                            if (s0 + C::SH < n_new) nu = u_begin + s0 + C::SH;
-                            else if (ci + 1 < nchunks) nu = C::A + ci * C::KB;
-                            else if (k + C::SP < gk1) nu = 0;
-                            if (nu >= 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0 + nu, C::TMA_BYTES);
+                        if constexpr (C::MW == 0) {
+                            mbar_wait(tma_bar, tparity);
+                            tparity ^= 1u;
+                            modulate2<C, C::NA>(ta, fbuf, gb0, gb1, csbase, csbase + CSZ, tk, gsub, np);
+                            named_sync<C::NA>(1);   // G-pairs complete; fbuf free; previous H-pass done
+                            if (ta == 0) {
+                                int nu = -1;
+                                if (s0 + C::SH < n_new) nu = u_begin + s0 + C::SH;
+                                else if (ci + 1 < nchunks) nu = C::A + ci * C::KB;
+                                else if (k + C::SP < gk1) nu = 0;
+                                if (nu >= 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0 + nu, C::TMA_BYTES);
+                            }
+                        } else {
+                            mbar_wait(&gfull[buf], (it >> 1) & 1);   // the modulators filled G[buf]
                         }
                         if (p < C::NP && sw < np) {
                             // horizontal FIR: 8 outputs (row r8, columns 8cg .. 8cg+7) of sample sw
@@ -231,6 +244,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                                     });
                                 });
                             });
+                            if constexpr (C::MW > 0) mbar_arrive(&gempty[buf]);   // G[buf] read
                             // transpose through this warp's shared-memory tile: lane (r8, cg) holds
                             // row r8 of columns 8cg..8cg+7; lane x needs rows 0..7 of column x.
                             // Stride 9 float2 per column: both directions are bank-conflict free.
@@ -243,11 +257,56 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                             __syncwarp();
                             const int slot = gsub % C::HROWS;   // 8 consecutive slots, no wrap
                             tmem_st16(tq + 2 * slot, acc);
+                        } else if constexpr (C::MW > 0) {
+                            mbar_arrive(&gempty[buf]);
                         }
                         if (s0 + C::SH >= n_new) {
                             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                             mbar_arrive(&full[q & 1]);
+                        }
+                    }
+                }
+            }
+        } else if (tid >= C::NA + C::NB) {
+            // ============================ MODULATORS (MW > 0) =================
+            // Alg. 1 L222-226 for both samples of a pass, one SH-row sub-step at a time, into the
+            // double-buffered G-pairs; they also own the TMA of f. They run up to two sub-steps
+            // ahead of the H-pass (gfull / gempty), which the (c, s) ring's 2 SH extra rows absorb.
+            if constexpr (C::MW > 0) {
+                const int tm = tid - C::NA - C::NB;
+                uint32_t tparity = 0;
+                int buf = 0, it = 0;
+                if (tm == 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0, C::TMA_BYTES);
+                for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
+                    const int np = min(C::SP, gk1 - k);
+                    float tk[2][C::D];
+#pragma unroll
+                    for (int s = 0; s < 2; ++s)
+#pragma unroll
+                        for (int c = 0; c < C::D; ++c)
+                            tk[s][c] = (c < a.d && s < np) ? __ldg(a.t + (long long)(k + s) * a.d + c) : 0.f;
+                    const int gs = pass * rows_per_pass;
+                    for (int ci = 0; ci < nchunks; ++ci) {
+                        const bool first_c = (ci == 0);
+                        const int u_begin = first_c ? 0 : C::A + (ci - 1) * C::KB;
+                        const int n_new = first_c ? C::A : C::KB;
+                        for (int s0 = 0; s0 < n_new; s0 += C::SH, buf ^= 1, ++it) {
+                            const int gsub = gs + u_begin + s0;
+                            if (it >= 2) mbar_wait(&gempty[buf], ((it - 2) >> 1) & 1);
+                            mbar_wait(tma_bar, tparity);
+                            tparity ^= 1u;
+                            modulate2<C, C::NM>(tm, fbuf, gbase + (2 * buf) * GSZ, gbase + (2 * buf + 1) * GSZ, csbase,
+                                                csbase + CSZ, tk, gsub, np);
+                            named_sync<C::NM>(2);   // fbuf consumed by every modulator
+                            if (tm == 0) {
+                                int nu = -1;
+                                if (s0 + C::SH < n_new) nu = u_begin + s0 + C::SH;
+                                else if (ci + 1 < nchunks) nu = C::A + ci * C::KB;
+                                else if (k + C::SP < gk1) nu = 0;
+                                if (nu >= 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0 + nu, C::TMA_BYTES);
+                            }
+                            mbar_arrive(&gfull[buf]);
                         }
                     }
                 }

@@ -15,7 +15,7 @@ from workloads.configs import random_image
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6])
 def test_config2_parity(variant):
     cfg = CONFIGS[2]
     f = make_image(cfg)
@@ -28,7 +28,7 @@ def test_config2_parity(variant):
     H.assert_gates(res)
 
 
-@pytest.mark.parametrize("variant", [2, 4, 5])
+@pytest.mark.parametrize("variant", [2, 4, 5, 6])
 @pytest.mark.parametrize("case", [(131, 77, 3, 5.0, 30, 17, 9, "full"), (70, 96, 3, 16.0, 40, 7, 2, "diag"),
                                   (40, 33, 3, 8.0, 20, 5, 4, "full")])
 def test_edge_parity(variant, case):
