@@ -10,10 +10,10 @@ the 8192x8192 scaling config; see DESIGN.md §7 for why). Inputs are resident
 in HBM when the timed region starts; `e2e` times bf_vec_filter_host (pinned
 host buffers, H2D + filter + D2H inside the timed region).
 
-N > 1 (torchrun, one rank per GPU, NCCL): `--mode bands` (default) splits the
-image into row bands with an r-row halo (no communication, strong scaling);
-`--mode samples` splits the M samples and sums the (d+1) accumulator planes
-with one NCCL reduce-scatter (strong scaling).
+N > 1 (torchrun, one rank per GPU, NCCL): `--mode samples` (default) splits the M
+samples and sums the (d+1) accumulator planes with one NCCL reduce-scatter
+(strong scaling); `--mode bands` splits the image into row bands with an r-row
+halo (no communication, strong scaling; DESIGN.md §8 compares the two).
 
 `--impl reference` times the CPU oracle (Algorithm 1 in fp64, OpenMP) on a
 bounded row band of the same workload on this host's cores.
@@ -42,7 +42,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="bands", choices=["bands", "samples"])
+    ap.add_argument("--mode", default="samples", choices=["bands", "samples"],
+                    help="N > 1 partition: samples (default; one NCCL reduce-scatter) or row bands (no "
+                         "communication, per-pass pipeline fill grows as the band shrinks)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 = library default)")

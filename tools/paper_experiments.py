@@ -87,6 +87,28 @@ def fig5(f, rows, nreal, t_list):
             p.close()
 
 
+def lab_bandwidth(rows, reps):
+    """sRGB <-> CIE-Lab transforms on the 8192^2 config-5 image: HBM-bound,
+    12 B read + 12 B written per pixel; reported against the measured copy bandwidth."""
+    from paper_1605_02164_b200 import lab_to_srgb, srgb_to_lab
+    f = torch.from_numpy(make_image(CONFIGS[5])).cuda()
+    out = torch.empty_like(f)
+    npix = f.shape[1] * f.shape[2]
+    peak = None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as fh:
+            peak = json.load(fh).get("hbm_gbs")
+    except Exception:
+        pass
+    for name, fn in (("srgb_to_lab", lambda: srgb_to_lab(f, out=out)), ("lab_to_srgb", lambda: lab_to_srgb(f, out=out))):
+        ms = timed(fn, reps)
+        gbs = 24.0 * npix / (ms / 1e3) / 1e9
+        row = {"experiment": "lab", "kernel": name, "pixels": npix, "ms": ms, "GB_per_s": gbs,
+               "hbm_peak_GB_per_s": peak, "frac": (gbs / peak) if peak else None}
+        print(json.dumps(row), flush=True)
+        rows.append(row)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="table1,fig5")
@@ -100,6 +122,8 @@ def main():
         table1(f, rows, a.reps)
     if "fig5" in a.which:
         fig5(f, rows, a.realisations, [25, 50, 100, 200, 300, 400])
+    if "lab" in a.which:
+        lab_bandwidth(rows, a.reps)
     if a.out:
         with open(a.out, "w") as fh:
             json.dump(rows, fh, indent=1)
