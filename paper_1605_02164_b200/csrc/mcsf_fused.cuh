@@ -60,10 +60,14 @@ struct Cfg {
     static constexpr int RING = 2 * KB + R;
     static constexpr int NIN = 8 + 2 * R;    // H-pass inputs per 8 outputs
     static constexpr int HITEMS = NP * SH * 4;     // H-pass items (pair, row, 8-column group)
+    // PM (pre-modulated, d = 8): the modulation writes every pair's G = (c f_q, s f_q) once, so the
+    // H-pass reads one float2 per tap input instead of (c, s) and f and an FMUL2 (the kernel is
+    // shared-memory-bandwidth bound at nine pairs, profiles/r01_v3_fused_c4_ncu.md)
+    static constexpr bool PM = (D == 8);
     // shared-memory carve-up (bytes, 128-aligned regions)
     static constexpr int SZ_F = SH * WIN * DP * 4;
-    static constexpr int SZ_CS = SH * MS * 8;
-    static constexpr int SZ_MF = D * SH * MSF * 4;
+    static constexpr int SZ_CS = PM ? NP * SH * MS * 8 : SH * MS * 8;
+    static constexpr int SZ_MF = PM ? 0 : D * SH * MSF * 4;
     static constexpr int SZ_HB = NP * HROWS * TX * 8;
     static constexpr int SZ_RING = RING * TX * 8;
     static constexpr int OFF_F = 0;
@@ -116,9 +120,16 @@ __device__ __forceinline__ void modulate(int ta, const float *fbuf, float2 *modc
         float s, c;
         __sincosf(th, &s, &c);
         const float2 cs = make_float2(c, s);
-        modcs[row * C::MS + j] = cs;
+        if constexpr (C::PM) {
+            modcs[row * C::MS + j] = cs;                                  // pair 0: Z
 #pragma unroll
-        for (int q = 0; q < C::D; ++q) modf[(q * C::SH + row) * C::MSF + j] = fv[q];
+            for (int q = 0; q < C::D; ++q)
+                modcs[((q + 1) * C::SH + row) * C::MS + j] = __fmul2_rn(cs, make_float2(fv[q], fv[q]));
+        } else {
+            modcs[row * C::MS + j] = cs;
+#pragma unroll
+            for (int q = 0; q < C::D; ++q) modf[(q * C::SH + row) * C::MSF + j] = fv[q];
+        }
         if (j >= C::R && j < C::R + C::TX) csring[((g0 + row) % C::RING) * C::TX + (j - C::R)] = cs;
     }
 }
@@ -135,7 +146,7 @@ __device__ __forceinline__ void hpass_item(const FusedArgs &a, const float2 *csr
         constexpr int jj = decltype(JJ)::value;
         const float4 c2 = *reinterpret_cast<const float4 *>(csrow + 2 * jj);
         float2 v[2] = {make_float2(c2.x, c2.y), make_float2(c2.z, c2.w)};
-        {
+        if constexpr (!C::PM) {
             const float2 f2 = *reinterpret_cast<const float2 *>(frow + 2 * jj);
             v[0] = __fmul2_rn(v[0], make_float2(f2.x, f2.x));
             v[1] = __fmul2_rn(v[1], make_float2(f2.y, f2.y));
@@ -165,9 +176,9 @@ __device__ __forceinline__ void hpass(int ta, const FusedArgs &a, const float2 *
         const int cg = (it / C::SH) & 3;
         const int p = it / (4 * C::SH);              // warp-uniform
         if (row >= n) continue;
-        const float2 *csrow = modcs + row * C::MS + cg * 8;
+        const float2 *csrow = modcs + ((C::PM ? p * C::SH : 0) + row) * C::MS + cg * 8;
         float2 *dst = hb + (p * C::HROWS + (g0 + row) % C::HROWS) * C::TX + cg * 8;
-        const float *frow = (p == 0) ? ones + cg * 8 : modf + ((p - 1) * C::SH + row) * C::MSF + cg * 8;
+        const float *frow = (C::PM || p == 0) ? ones + cg * 8 : modf + ((p - 1) * C::SH + row) * C::MSF + cg * 8;
         hpass_item<C>(a, csrow, frow, dst);
     }
 }
