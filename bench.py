@@ -218,7 +218,7 @@ def run_reference(args, cfg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(cfg, args.gpus, args.mode),
+        "config": config_dict(cfg, args.gpus, args.mode, engine="fir"),
         "cpu_baseline": {"value": value, "unit": "pixel*samples/s", "cores": info["threads"],
                          "kind": "oracle",
                          "sample": f"output rows {info['rows']} x {cfg.W} cols, first {samples} of "
