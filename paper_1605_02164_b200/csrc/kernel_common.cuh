@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <utility>
 
 #include "internal.h"
@@ -70,6 +71,20 @@ __device__ __forceinline__ void static_for(F &&f) {
 
 __device__ __forceinline__ float2 ffma2(float w, float2 v, float2 acc) {
     return __ffma2_rn(make_float2(w, w), v, acc);
+}
+
+// Opt a kernel into `bytes` of dynamic shared memory once per device (the attribute is per
+// function and per device; one process may drive several devices through the C ABI).
+template <class K>
+cudaError_t ensure_smem_attr(K kernel, size_t bytes, std::atomic<uint64_t> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {

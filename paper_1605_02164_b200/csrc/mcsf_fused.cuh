@@ -325,12 +325,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) mcsf_fused_kernel(const __grid
 template <class C>
 cudaError_t launch_cfg(const FusedArgs &a, dim3 grid, cudaStream_t s) {
     auto k = mcsf_fused_kernel<C>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    const cudaError_t e = ensure_smem_attr(k, C::SMEM, attr);
+    if (e != cudaSuccess) return e;
     k<<<grid, C::NT, C::SMEM, s>>>(a);
     return cudaGetLastError();
 }

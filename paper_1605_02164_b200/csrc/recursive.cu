@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include "internal.h"
+#include "kernel_common.cuh"
 
 namespace bfvec {
 namespace {
@@ -348,12 +349,10 @@ __global__ void __launch_bounds__(32 * NP) rec_col_kernel(const __grid_constant_
 template <int NP>
 cudaError_t launch_np(const RecArgs &a, cudaStream_t s) {
     const size_t smem = RowSmem<NP>::BYTES;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(rec_row_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+    static std::atomic<uint64_t> attr{0};
+    {
+        const cudaError_t e = ensure_smem_attr(rec_row_kernel<NP>, smem, attr);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     dim3 grow((a.H + kT - 1) / kT, a.nb), gcol((a.W + kT - 1) / kT, a.nb);
     rec_row_kernel<NP><<<grow, 32 * NP, smem, s>>>(a);

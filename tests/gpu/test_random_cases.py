@@ -1,0 +1,63 @@
+"""Seeded random small cases over the whole option space (shape, d, sigma_s, N, M, C, engine,
+spatial kernel, sampler, variant, schedule): the CUDA path against the oracle under the usual
+gates (tests/gpu/helpers.py). A fixed list drawn from numpy's default_rng(2026), so a failure
+reproduces by its case index."""
+import numpy as np
+import pytest
+
+from oracle import draws, native
+from oracle import plan as oplan
+from tests.gpu import helpers as H
+from workloads.configs import random_image, small_config
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(n=28):
+    rng = np.random.default_rng(2026)
+    out = []
+    for i in range(n):
+        d = int(rng.choice([1, 2, 3, 3, 3, 4, 5, 8]))
+        Hh = int(rng.integers(1, 90))
+        W = int(rng.integers(1, 110))
+        s = float(rng.choice([0.5, 1.0, 2.2, 3.7, 5.0, 8.0, 12.0, 16.0]))
+        N = int(rng.choice([4, 10, 20, 40]))
+        M = int(rng.integers(1, 12))
+        engine = int(rng.random() < 0.3)
+        spatial = "gaussian" if engine == 1 else str(rng.choice(["gaussian", "gaussian", "box", "hat"]))
+        sampler = int(rng.random() < 0.3)
+        variant = int(rng.choice([0, 0, 1, 2, 4]))
+        tile, groups = int(rng.choice([0, 16, 48])), int(rng.choice([0, 1, 3]))
+        full = bool(rng.random() < 0.5)
+        out.append((i, Hh, W, d, s, N, M, engine, spatial, sampler, variant, tile, groups, full))
+    return out
+
+
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: f"case{c[0]}")
+def test_random_case(case):
+    i, Hh, W, d, s, N, M, engine, spatial, sampler, variant, tile, groups, full = case
+    if engine == 0 and int(np.ceil(3 * s - 1e-12)) > 64:
+        pytest.skip("FIR radius > 64")
+    rng = np.random.default_rng(i)
+    if full:
+        A = rng.normal(size=(d, d))
+        C = 40.0 ** 2 * (A @ A.T / d + np.eye(d))
+    else:
+        C = np.diag(rng.uniform(20.0, 60.0, d) ** 2)
+    cfg = small_config(d=d, H=Hh, W=W, sigma_s=s, N=N, M=M, seed=100 + i, C=C)
+    f = random_image(Hh, W, d, seed=i, smooth=bool(i % 2))
+    Q, a = oplan.diagonalize(C)
+    Y = (draws.y_draws if sampler == 0 else draws.stratified_y_draws)(cfg.seed, M, d, N)
+    S_o, P_o, Z_o = native.mcsf_full(f, Q, a, N, Y, s, spatial="deriche" if engine == 1 else spatial)
+    from paper_1605_02164_b200 import Plan
+    p = Plan(Hh, W, d, s, C, N, M, cfg.seed)
+    p.set_option("engine", engine)
+    p.set_option("spatial_kernel", oplan.SPATIAL_KINDS[spatial])
+    p.set_option("sampler", sampler)
+    p.set_option("variant", variant)
+    p.set_option("tile_rows", tile)
+    p.set_option("groups", groups)
+    p.sample_freqs()
+    res = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
+    print(case, res)
+    H.assert_gates(res)
