@@ -42,9 +42,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="samples", choices=["bands", "samples"],
-                    help="N > 1 partition: samples (default; one NCCL reduce-scatter) or row bands (no "
-                         "communication, per-pass pipeline fill grows as the band shrinks)")
+    ap.add_argument("--mode", default="samples", choices=["bands", "samples", "samples-p2p"],
+                    help="N > 1 partition: samples (default; one NCCL reduce-scatter), samples-p2p (the "
+                         "fused kernel stores finished partials into the band owners' peer memory), or row "
+                         "bands (no communication, per-pass pipeline fill grows as the band shrinks)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 = library default)")
@@ -255,7 +256,8 @@ def run_ours(args, cfg):
     plan.sample_freqs()
 
     # this rank's work
-    if world == 1 or args.mode == "samples":
+    sampled = args.mode in ("samples", "samples-p2p")
+    if world == 1 or sampled:
         y0, y1, s0, s1 = 0, cfg.H, 0, cfg.H
     else:
         y0, y1 = shard.band(cfg.H, world, rank)
@@ -264,11 +266,12 @@ def run_ours(args, cfg):
     f = f_host.to(dev)
     rows = y1 - y0
     out = torch.empty((cfg.d, rows, cfg.W), dtype=torch.float32, device=dev)
-    k0, k1 = shard.sample_range(cfg.M, world, rank) if args.mode == "samples" else (0, cfg.M)
-    if args.mode == "samples" and world > 1:
+    k0, k1 = shard.sample_range(cfg.M, world, rank) if sampled else (0, cfg.M)
+    if sampled and world > 1:
         y0, y1 = shard.sample_band(cfg.H, world, rank)
         rows = y1 - y0
         out = torch.empty((cfg.d, rows, cfg.W), dtype=torch.float32, device=dev)
+    slots = shard.P2PSlots(plan, world, rank) if (args.mode == "samples-p2p" and world > 1) else None
 
     stream = torch.cuda.current_stream()
     launches_per_step = 0
@@ -280,6 +283,9 @@ def run_ours(args, cfg):
             launches_per_step = plan.info("launches_per_filter")   # FIR: pad, fused, diag reset, normalise
         elif args.mode == "bands":
             shard.filter_bands(plan, f, s0, out=out)
+            launches_per_step = 4
+        elif slots is not None:
+            shard.filter_samples_p2p(plan, f, slots)   # pad, fused (+ peer stores), diag reset, normalise
             launches_per_step = 4
         else:
             shard.filter_samples(plan, f)   # partial (pad, fused, finalise), NCCL reduce-scatter, normalise

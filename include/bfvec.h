@@ -126,6 +126,34 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t plan, const float *f, int k0, in
                                   int rows_per_band, void *stream);
 
 /*
+ * bf_vec_filter_partial_p2p -- sample sharding with the exchange fused into the MC kernel: this
+ * rank (of `world`, one process per GPU) filters samples [k0, k1) in `slots_per_rank` sample
+ * groups, and the LAST pass of every group stores its finished partial tile rows directly into
+ * the receive slots of the rank owning each row band (peer memory over NVLink), while other CTAs
+ * are still computing -- the reduce-scatter of bf_vec_filter_partial + NCCL without a separate
+ * collective. After every rank's call has completed (e.g. a barrier on the stream), each owner
+ * sums and normalises its slots with bf_vec_normalize_slots.
+ *   peer_slots      host array of `world` device pointers: rank b's receive buffer of
+ *                   world * slots_per_rank slots, slot (r * slots_per_rank + g) holding
+ *                   (D+1, H/world, W) fp32 planes (D = bf_vec_plan_info "kernel_D"; P' centred,
+ *                   Z last), written for band b = rows [b H/world, (b+1) H/world)
+ *   slots_per_rank  >= 1 and <= k1 - k0 (every group gets a sample)
+ * Requires H % world == 0, the default FIR engine on the v6 kernel (d <= 3, 10 < r <= 48), no
+ * colorspace (else BF_E_UNSUPPORTED). The caller maps peers' buffers (CUDA IPC).
+ */
+bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t plan, const float *f, int k0, int k1,
+                                      float *const *peer_slots, int world, int rank,
+                                      int slots_per_rank, void *stream);
+
+/*
+ * bf_vec_normalize_slots -- Alg. 1 L231 on a receive buffer of bf_vec_filter_partial_p2p:
+ * out_c = (sum_s P'_c,s) / (sum_s Z_s) + mu_c for rows [row0, row1) (the owner's band), summing
+ * the nslots slots in order (deterministic). slots: device (nslots, D+1, row1-row0, W).
+ */
+bf_status_t bf_vec_normalize_slots(bf_vec_plan_t plan, const float *slots, int nslots, int row0,
+                                   int row1, float *out_band, void *stream);
+
+/*
  * bf_vec_normalize -- Alg. 1: out_c = P_c / Z for rows [row0, row1).
  *   PZ_band   device (d+1, row1-row0, W) block as written by filter_partial
  *             (and summed over shards)

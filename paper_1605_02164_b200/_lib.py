@@ -26,6 +26,8 @@ SIGNATURES = {
     "bf_vec_diag": ([_P, _P, _P], _I),
     "bf_vec_mse_sweep": ([_P, _P, _P, _I, _P, _I, _P, _P, _P], _I),
     "bf_vec_srgb_to_lab": ([_P, _P, ctypes.c_longlong, _P], _I),
+    "bf_vec_filter_partial_p2p": ([_P, _P, _I, _I, _P, _I, _I, _I, _P], _I),
+    "bf_vec_normalize_slots": ([_P, _P, _I, _I, _I, _P, _P], _I),
     "bf_vec_lab_to_srgb": ([_P, _P, ctypes.c_longlong, _P], _I),
     "bf_vec_set_option": ([_P, ctypes.c_char_p, _D], _I),
     "bf_vec_plan_info": ([_P, ctypes.c_char_p, _P], _I),

@@ -135,6 +135,23 @@ class Plan:
             raise ValueError("PZ must hold (d+1)*H*W floats")
         return PZ
 
+    def filter_partial_p2p(self, f, k0, k1, peer_slots, world, rank, slots_per_rank, stream=None):
+        """bf_vec_filter_partial_p2p: peer_slots = list of `world` device pointers (ints)."""
+        arr = (ctypes.c_void_p * world)(*[ctypes.c_void_p(int(x)) for x in peer_slots])
+        check(self._lib.bf_vec_filter_partial_p2p(self._h, _dev(f, (self.d, self.H, self.W), "f"), int(k0), int(k1),
+                                                  arr, int(world), int(rank), int(slots_per_rank),
+                                                  _stream_ptr(stream)), "bf_vec_filter_partial_p2p")
+
+    def normalize_slots(self, slots_ptr, nslots, row0, row1, out=None, device=None, stream=None):
+        """bf_vec_normalize_slots on a raw device pointer to (nslots, D+1, rows, W) slots."""
+        rows = int(row1) - int(row0)
+        if out is None:
+            out = torch.empty((self.d, rows, self.W), dtype=torch.float32, device=device or "cuda")
+        check(self._lib.bf_vec_normalize_slots(self._h, ctypes.c_void_p(int(slots_ptr)), int(nslots), int(row0),
+                                               int(row1), _dev(out, (self.d, rows, self.W), "out"),
+                                               _stream_ptr(stream)), "bf_vec_normalize_slots")
+        return out
+
     def normalize(self, PZ_band, row0, row1, out=None, stream=None):
         rows = int(row1) - int(row0)
         if PZ_band.numel() != (self.d + 1) * rows * self.W:

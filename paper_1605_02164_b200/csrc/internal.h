@@ -31,6 +31,12 @@ struct alignas(64) FusedArgs {
     const float *t;       // (M, d) frequency table, fp32
     float *pz;            // (groups, D+1, out_rows, W): planes 0..D-1 = P' (centred), D = Z
     float w[kMaxR + 1];   // normalised taps w[|m|], zero beyond the plan radius
+    // peer-slot output (bf_vec_filter_partial_p2p; v6 kernel only): when p2p_world > 0 the LAST
+    // pass of every sample group stores its tile rows straight into the receive slots of the rank
+    // that owns each row band: peer[owner] + ((p2p_rank * groups + g) * (D+1) + plane) * p2p_rpb * W
+    // + (row - owner * p2p_rpb) * W + x, over NVLink while other CTAs are still computing.
+    float *peer[8];
+    int p2p_world, p2p_rank, p2p_rpb;
 };
 
 struct PadMu {

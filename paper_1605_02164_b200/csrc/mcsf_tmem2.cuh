@@ -385,9 +385,25 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     mbar_arrive(&empty[q & 1]);
                     if (active && xok) {
+                        if (a.p2p_world > 0 && k + C::SP >= gk1) {
+                            // last pass of the group: the finished partial goes to the band owner's
+                            // receive slot (peer memory over NVLink), not back to the local tile
 #pragma unroll
-                        for (int o = 0; o < OR; ++o)
-                            if (cy + o < ty1) dst[(long long)o * a.W] = tot[o];
+                            for (int o = 0; o < OR; ++o) {
+                                const int row = cy + o;
+                                if (row < ty1) {
+                                    const int owner = row / a.p2p_rpb;
+                                    float *slot = a.peer[owner] +
+                                                  ((long long)(a.p2p_rank * a.groups + g) * (C::D + 1) + plane) *
+                                                      a.p2p_rpb * a.W;
+                                    slot[(long long)(row - owner * a.p2p_rpb) * a.W + x] = tot[o];
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int o = 0; o < OR; ++o)
+                                if (cy + o < ty1) dst[(long long)o * a.W] = tot[o];
+                        }
                     }
                 }
             }

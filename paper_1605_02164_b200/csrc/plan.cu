@@ -276,11 +276,17 @@ bf_status_t encode_tmap(CUtensorMap *map, float *base, int dp, int Wp, int Hp, i
 }
 
 // one fused launch: output rows [out_row0, out_row0+out_rows), samples [k0, k1)
+struct P2POut {
+    float *const *peer;   // world receive-slot bases (device pointers), or null for local partials
+    int world, rank, slots;
+};
+
 bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_row0, int out_row0,
-                      int out_rows, int k0, int k1, cudaStream_t s, int *groups_out) {
+                      int out_rows, int k0, int k1, cudaStream_t s, int *groups_out, const P2POut *p2p = nullptr) {
     if (!p->kinfo_ok) return BF_E_UNSUPPORTED;   // r > 64 or no compiled instance: engine 1 only
     int tile_rows = 0, groups = 1;
     choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups);
+    if (p2p) groups = p2p->slots;   // one receive slot per (rank, group) on every owner
     const KernelInfo &ki = p->kinfo;
     const size_t need = sizeof(float) * (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;
     bf_status_t st = ensure_pz(p, need);
@@ -314,6 +320,12 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
     a.t = p->dt;
     a.pz = p->dpz;
     for (int i = 0; i <= kMaxR; ++i) a.w[i] = (i <= p->r) ? p->taps[i] : 0.f;
+    if (p2p) {
+        for (int i = 0; i < p2p->world; ++i) a.peer[i] = p2p->peer[i];
+        a.p2p_world = p2p->world;
+        a.p2p_rank = p2p->rank;
+        a.p2p_rpb = p->H / p2p->world;
+    }
     dim3 grid((p->W + kTX - 1) / kTX, (out_rows + tile_rows - 1) / tile_rows, groups);
     p->last_tile_rows = tile_rows;
     p->last_groups = groups;
@@ -651,6 +663,40 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k
     BF_CUDA(launch_finalize_partial(p->dpz, groups, p->engine == 1 ? p->d : p->kinfo.D, p->d, p->H, p->W, p->mu,
                                     rows_per_band, PZ, s));
     p->last_launches = 3;
+    p->last = s;
+    return BF_OK;
+}
+
+bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t p, const float *f, int k0, int k1, float *const *peer_slots,
+                                      int world, int rank, int slots_per_rank, void *stream) {
+    if (!valid_plan(p) || !f || !peer_slots) return BF_E_ARG;
+    if (world < 1 || world > 8 || rank < 0 || rank >= world || slots_per_rank < 1) return BF_E_ARG;
+    if (k0 < 0 || k1 > p->M || k1 - k0 < slots_per_rank) return BF_E_ARG;   // every group non-empty
+    for (int i = 0; i < world; ++i)
+        if (!peer_slots[i]) return BF_E_ARG;
+    if (p->device < 0 || !p->sampled) return BF_E_STATE;
+    if (p->H % world != 0 || p->engine != 0 || p->lab || !p->kinfo_ok || p->kinfo.variant != 4)
+        return BF_E_UNSUPPORTED;
+    const P2POut o{peer_slots, world, rank, slots_per_rank};
+    int groups = 1;
+    bf_status_t st = run_fused(p, f, p->H, 0, 0, p->H, k0, k1, S(stream), &groups, &o);
+    if (st != BF_OK) return st;
+    p->last_launches = 2;
+    p->last = S(stream);
+    return BF_OK;
+}
+
+bf_status_t bf_vec_normalize_slots(bf_vec_plan_t p, const float *slots, int nslots, int row0, int row1,
+                                   float *out_band, void *stream) {
+    if (!valid_plan(p) || !slots || !out_band || nslots < 1) return BF_E_ARG;
+    if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
+    if (p->device < 0 || !p->kinfo_ok) return BF_E_STATE;
+    cudaStream_t s = S(stream);
+    fill_mu(p);
+    BF_CUDA(launch_diag_reset(p->ddiag, s));
+    BF_CUDA(launch_normalize_groups(slots, nslots, p->kinfo.D, p->d, row1 - row0, p->W, p->mu, out_band, p->ddiag,
+                                    1.0f / p->M, (float)p->z_floor, s));
+    p->last_launches = 2;
     p->last = s;
     return BF_OK;
 }

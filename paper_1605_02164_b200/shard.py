@@ -6,6 +6,10 @@ Two ways to split one image over G ranks:
   [g H / G, (g+1) H / G) from an input slab that holds every row within r of its
   band (half-sample reflection at the true image edges, reading R1) through
   `bf_vec_filter_rows`. No communication.
+* **sample shards, fused exchange** (`filter_samples_p2p`): as below, but the fused kernel's
+  last pass stores each finished partial tile straight into the band owner's receive slot in
+  peer memory (CUDA IPC mapping, NVLink), so the exchange overlaps the computation of the other
+  CTAs and there is no separate collective; owners normalise their slots.
 * **sample shards** (`filter_samples`): rank g owns samples
   [floor(g M / G), floor((g+1) M / G)) (reading R10), computes raw (P, Z) sums over
   the whole image with `bf_vec_filter_partial` in band-major layout, one
@@ -92,6 +96,73 @@ def filter_samples(plan, f: torch.Tensor, group=None, partial_fn=None, normalize
     return normalize_fn(PZ_band, y0, y1), y0, y1
 
 
+class P2PSlots:
+    """This rank's receive buffer for `bf_vec_filter_partial_p2p` (world * slots_per_rank slots of
+    (D+1, H/world, W) fp32) and the device pointers of every rank's buffer, mapped through CUDA IPC
+    (cuda-python runtime bindings; the buffer is a plain cudaMalloc so its IPC handle covers it
+    exactly). world == 1 needs no IPC."""
+
+    def __init__(self, plan, world: int, rank: int, slots_per_rank: int = 4, group=None):
+        from cuda.bindings import runtime as rt
+        self._rt = rt
+        self.world, self.rank, self.slots_per_rank = world, rank, slots_per_rank
+        D = plan.info("kernel_D")
+        if plan.H % world:
+            raise ValueError("P2P sample sharding needs H divisible by the world size")
+        self.rows = plan.H // world
+        nbytes = world * slots_per_rank * (D + 1) * self.rows * plan.W * 4
+        err, ptr = rt.cudaMalloc(nbytes)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise MemoryError(f"cudaMalloc({nbytes}) failed: {err}")
+        self.ptr = int(ptr)
+        self._opened = []
+        if world == 1:
+            self.peers = [self.ptr]
+            return
+        err, h = rt.cudaIpcGetMemHandle(ptr)
+        if err != rt.cudaError_t.cudaSuccess:
+            raise RuntimeError(f"cudaIpcGetMemHandle failed: {err}")
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(h.reserved), group=group)
+        peers = []
+        for r, hb in enumerate(handles):
+            if r == rank:
+                peers.append(self.ptr)
+                continue
+            hh = rt.cudaIpcMemHandle_t()
+            hh.reserved = hb
+            err, pp = rt.cudaIpcOpenMemHandle(hh, rt.cudaIpcMemLazyEnablePeerAccess)
+            if err != rt.cudaError_t.cudaSuccess:
+                raise RuntimeError(f"cudaIpcOpenMemHandle(rank {r}) failed: {err}")
+            self._opened.append(pp)
+            peers.append(int(pp))
+        self.peers = peers
+
+    def close(self):
+        for pp in self._opened:
+            self._rt.cudaIpcCloseMemHandle(pp)
+        self._opened = []
+        if self.ptr:
+            self._rt.cudaFree(self.ptr)
+            self.ptr = 0
+
+
+def filter_samples_p2p(plan, f: torch.Tensor, slots: P2PSlots, group=None):
+    """Sample sharding with the exchange fused into the MC kernel: partial sums over this rank's
+    samples are stored by the kernel's last pass straight into the band owners' receive slots
+    (NVLink peer stores), then -- once every rank's kernel has completed -- each rank normalises
+    its own band from its slots. Returns (out_band, y0, y1)."""
+    world, rank = slots.world, slots.rank
+    k0, k1 = sample_range(plan.M, world, rank)
+    plan.filter_partial_p2p(f, k0, k1, slots.peers, world, rank, slots.slots_per_rank)
+    if world > 1:
+        torch.cuda.current_stream().synchronize()   # this rank's peer stores are complete ...
+        dist.barrier(group)                          # ... and so are everyone else's
+    y0 = rank * slots.rows
+    y1 = y0 + slots.rows
+    return plan.normalize_slots(slots.ptr, world * slots.slots_per_rank, y0, y1, device=f.device), y0, y1
+
+
 def gather_bands(out_band: torch.Tensor, H: int, group=None, band_fn=band) -> torch.Tensor:
     """All-gather the per-rank bands into the full (d, H, W) image (for checking)."""
     world = dist.get_world_size(group)
@@ -113,4 +184,4 @@ def sample_band(H: int, world: int, rank: int) -> tuple:
 
 
 __all__ = ["band", "reflect", "slab_for_band", "sample_range", "band_layout", "filter_bands",
-           "filter_samples", "gather_bands", "sample_band"]
+           "filter_samples", "P2PSlots", "filter_samples_p2p", "gather_bands", "sample_band"]

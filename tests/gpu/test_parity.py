@@ -229,3 +229,23 @@ def test_direct_small_nondiagonal():
     g = p.direct(torch.from_numpy(f).cuda()).cpu().numpy()
     o = native.direct_full(f, cfg.C_array, cfg.sigma_s)
     assert np.abs(g - o).max() < 1e-3
+
+
+def test_p2p_sample_exchange_world1_matches_filter():
+    """bf_vec_filter_partial_p2p + bf_vec_normalize_slots on one rank (the peer table is this
+    rank's own receive buffer): the same result as bf_vec_filter up to fp32 summation order."""
+    from paper_1605_02164_b200 import shard
+    cfg = CONFIGS[2]
+    f = torch.from_numpy(make_image(cfg)).cuda()
+    p = H.gpu_plan(cfg)
+    ref = p.filter(f).cpu().numpy()
+    Z = p.filter_partial(f, 0, cfg.M).cpu().numpy().reshape(cfg.d + 1, cfg.H, cfg.W)[cfg.d]
+    slots = shard.P2PSlots(p, 1, 0, slots_per_rank=4)
+    try:
+        out, y0, y1 = shard.filter_samples_p2p(p, f, slots)
+        got = out.cpu().numpy()
+    finally:
+        slots.close()
+    assert (y0, y1) == (0, cfg.H)
+    ok = Z / cfg.M >= H.Z_FLOOR
+    assert np.abs(got - ref)[:, ok].max() < 2e-3
