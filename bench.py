@@ -285,10 +285,10 @@ def run_ours(args, cfg):
             shard.filter_bands(plan, f, s0, out=out)
             launches_per_step = 4
         elif slots is not None:
-            shard.filter_samples_p2p(plan, f, slots)   # pad, fused (+ peer stores), diag reset, normalise
+            shard.filter_samples_p2p(plan, f, slots, out=out)   # pad, fused (+ peer stores), diag reset, normalise
             launches_per_step = 4
         else:
-            shard.filter_samples(plan, f)   # partial (pad, fused, finalise), NCCL reduce-scatter, normalise
+            shard.filter_samples(plan, f, out=out)   # partial (pad, fused, finalise), NCCL reduce-scatter, normalise
             launches_per_step = 5
 
     flush = None

@@ -70,7 +70,7 @@ def filter_bands(plan, slab: torch.Tensor, slab_row0: int, group=None, out=None)
     return plan.filter_rows(slab, slab_row0, y0, y1, out=out), y0, y1
 
 
-def filter_samples(plan, f: torch.Tensor, group=None, partial_fn=None, normalize_fn=None):
+def filter_samples(plan, f: torch.Tensor, group=None, partial_fn=None, normalize_fn=None, out=None):
     """Sample sharding: partial sums over this rank's samples, one reduce-scatter,
     normalisation of this rank's band. Returns (out_band, y0, y1).
 
@@ -85,7 +85,7 @@ def filter_samples(plan, f: torch.Tensor, group=None, partial_fn=None, normalize
     if partial_fn is None:
         partial_fn = lambda f_, a, b, rows: plan.filter_partial(f_, a, b, rows_per_band=rows)  # noqa: E731
     if normalize_fn is None:
-        normalize_fn = plan.normalize
+        normalize_fn = lambda PZb, a, b: plan.normalize(PZb, a, b, out=out)  # noqa: E731
     PZ = partial_fn(f, k0, k1, rpb).reshape(-1)
     PZ_band = torch.empty(counts[rank], dtype=PZ.dtype, device=PZ.device)
     dist.reduce_scatter(PZ_band, list(torch.split(PZ, counts)), op=dist.ReduceOp.SUM, group=group)
@@ -147,7 +147,7 @@ class P2PSlots:
             self.ptr = 0
 
 
-def filter_samples_p2p(plan, f: torch.Tensor, slots: P2PSlots, group=None):
+def filter_samples_p2p(plan, f: torch.Tensor, slots: P2PSlots, group=None, out=None):
     """Sample sharding with the exchange fused into the MC kernel: partial sums over this rank's
     samples are stored by the kernel's last pass straight into the band owners' receive slots
     (NVLink peer stores), then -- once every rank's kernel has completed -- each rank normalises
@@ -160,7 +160,7 @@ def filter_samples_p2p(plan, f: torch.Tensor, slots: P2PSlots, group=None):
         dist.barrier(group)                          # ... and so are everyone else's
     y0 = rank * slots.rows
     y1 = y0 + slots.rows
-    return plan.normalize_slots(slots.ptr, world * slots.slots_per_rank, y0, y1, device=f.device), y0, y1
+    return plan.normalize_slots(slots.ptr, world * slots.slots_per_rank, y0, y1, out=out, device=f.device), y0, y1
 
 
 def gather_bands(out_band: torch.Tensor, H: int, group=None, band_fn=band) -> torch.Tensor:
