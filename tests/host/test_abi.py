@@ -108,3 +108,39 @@ def test_options_validate_without_gpu():
     for name, v in [("engine", 2), ("spatial_kernel", 5), ("rec_batch", -1), ("no_such_option", 1)]:
         with pytest.raises(BfVecError):
             p.set_option(name, v)
+
+
+def test_new_entry_points_validate_arguments_without_gpu():
+    """bf_vec_mse_sweep / _filter_partial_p2p / _normalize_slots / colour transforms reject bad
+    arguments before touching a device (no GPU in the CPU suite)."""
+    import ctypes
+    from paper_1605_02164_b200 import _lib
+    lib = _lib.load()
+    assert lib.bf_vec_srgb_to_lab(None, None, 10, None) == -1
+    assert lib.bf_vec_lab_to_srgb(None, None, 10, None) == -1
+    h = ctypes.c_void_p()
+    C = np.eye(3) * 100.0
+    assert lib.bf_vec_plan(16, 16, 3, 1.0, C.ctypes.data_as(ctypes.c_void_p), 10, 4, 0, ctypes.byref(h)) == 0
+    try:
+        seeds = (ctypes.c_uint64 * 1)(1)
+        tl = (ctypes.c_int * 2)(2, 1)                       # not increasing
+        mse = (ctypes.c_double * 2)()
+        dummy = ctypes.c_void_p(16)
+        assert lib.bf_vec_mse_sweep(h, dummy, dummy, 1, seeds, 2, tl, mse, None) == -1
+        peers = (ctypes.c_void_p * 1)(16)
+        assert lib.bf_vec_filter_partial_p2p(h, dummy, 0, 4, peers, 9, 0, 1, None) == -1      # world > 8
+        assert lib.bf_vec_filter_partial_p2p(h, dummy, 0, 2, peers, 1, 0, 3, None) == -1      # slots > samples
+        assert lib.bf_vec_filter_partial_p2p(h, dummy, 0, 4, peers, 1, 0, 2, None) == -6      # not sampled yet
+        assert lib.bf_vec_normalize_slots(h, dummy, 0, 0, 4, dummy, None) == -1
+    finally:
+        lib.bf_vec_plan_destroy(h)
+
+
+def test_plan_info_reports_every_documented_key():
+    from paper_1605_02164_b200 import Plan
+    p = Plan(16, 16, 3, 2.0, np.eye(3) * 100.0, 10, 4, 0)
+    for k in ["radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas", "launches_per_filter",
+              "smem_bytes", "threads", "kernel_D", "kernel_R", "regs", "occupancy", "alias", "variant",
+              "spatial_kernel", "engine", "rec_batch", "fir_supported", "sampler", "colorspace"]:
+        p.info(k)
+    assert p.info("radius") == 6 and p.info("M") == 4
