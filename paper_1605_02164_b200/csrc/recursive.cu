@@ -111,7 +111,7 @@ template <int NP>
 struct RowSmem {
     static constexpr int D = NP - 1;
     static constexpr int TILE = kT * (kT + 1);           // floats per padded 32 x 32 tile
-    static constexpr int OB = (NP <= 6) ? 2 : 1;         // partial-tile buffers (227 KB budget)
+    static constexpr int OB = 1;                          // partial-tile buffers: one (3 CTAs per SM at d = 3)
     static constexpr int OFF_CS = 2 * D * TILE;          // fs[2][D] tiles first
     static constexpr int OFF_OB = OFF_CS + 2 * TILE;     // cs: TILE float2
     static constexpr size_t BYTES = sizeof(float) * (size_t)(OFF_OB + OB * 2 * NP * TILE);
