@@ -148,12 +148,15 @@ int sm_count() {
 // Free device memory for the scratch-budget heuristics, queried once per plan: cudaMemGetInfo
 // is a driver round trip that occasionally stalls the host for milliseconds, which showed up as
 // outliers in the event-timed short launches.
+// The value is the memory available to this plan's scratch: free memory plus what the plan
+// already holds, both at the first query -- so later budgets do not drift as the plan allocates.
 size_t free_memory(bf_vec_plan_t p) {
     if (p->free_mem == 0) {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
         cudaGetLastError();
-        p->free_mem = free_b ? free_b : 1;
+        const size_t avail = free_b ? free_b + p->pz_bytes + p->drec_bytes : 0;
+        p->free_mem = avail ? avail : 1;
     }
     return p->free_mem > 1 ? p->free_mem : 0;
 }
@@ -174,7 +177,7 @@ void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows
     int bt = KB, bg = 1;
     const int rmax = (out_rows + KB - 1) / KB * KB;
     const size_t free_b = free_memory(p);
-    const double pz_budget = std::min(0.25 * (double)(free_b + p->pz_bytes), 24.0 * 1073741824.0);
+    const double pz_budget = std::min(0.25 * (double)free_b, 24.0 * 1073741824.0);
     for (int ty = KB;; ty *= 2) {
         const int t = std::min(ty, rmax);
         const int ny = (out_rows + t - 1) / t;
@@ -434,7 +437,7 @@ bf_status_t run_recursive(bf_vec_plan_t p, const float *f, int k0, int k1, cudaS
     // per sample in flight: y1 + y2 (2 x 2(d+1) planes) + one partial group ((d+1) planes)
     const double per = 4.0 * px * (4.0 * (p->d + 1) + (p->d + 1));
     const size_t free_b = free_memory(p);
-    int nb = (int)std::max(1.0, std::min<double>(256.0, 0.4 * (free_b + p->drec_bytes + p->pz_bytes) / per));
+    int nb = (int)std::max(1.0, std::min<double>(256.0, 0.4 * (double)free_b / per));
     if (p->force_batch > 0) nb = p->force_batch;
     nb = std::min(nb, ns);
     bf_status_t st = ensure_rec_scratch(p, nb);
