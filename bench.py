@@ -264,6 +264,10 @@ def run_ours(args, cfg):
         s0, s1 = shard.slab_for_band(cfg.H, r, y0, y1)
     f_host = torch.from_numpy(make_image_rows(cfg, s0, s1))
     f = f_host.to(dev)
+    torch.cuda.synchronize()
+    # run on a created (capturable) stream: bf_vec_filter then replays its launch sequence as one
+    # CUDA graph (option "graph"); the legacy default stream cannot be captured
+    torch.cuda.set_stream(torch.cuda.Stream(device=dev))
     rows = y1 - y0
     out = torch.empty((cfg.d, rows, cfg.W), dtype=torch.float32, device=dev)
     k0, k1 = shard.sample_range(cfg.M, world, rank) if sampled else (0, cfg.M)

@@ -261,6 +261,10 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 ("any arbitrary spatial filter (such as a box or hat filter)";
  *                 DESIGN.md reading R15); taps are normalised to sum 1. Applies to the MC
  *                 filter and to bf_vec_direct.
+ *   "graph"       1 (default): bf_vec_filter on a non-default stream captures its launch sequence
+ *                 into a CUDA graph on the second call with the same (f, out, stream) and
+ *                 options, and replays it afterwards (one cudaGraphLaunch per call); any option
+ *                 change or bf_vec_sample_freqs re-captures. 0: always launch eagerly.
  *   "profile"     1: record CUDA events around every fused-kernel launch on the
  *                 launching stream (read back with bf_vec_plan_info
  *                 "fused_ns_total" / "fused_calls"); 0: off. Setting it resets the totals.
@@ -273,7 +277,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value
  *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
  *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
  *   "regs", "occupancy", "alias", "variant", "spatial_kernel", "engine", "rec_batch" (last batch
- *   size), "fir_supported" (r <= 64), "sampler", "colorspace", and (option "profile") "fused_ns_total",
+ *   size), "fir_supported" (r <= 64), "sampler", "colorspace", "graph", "graph_ready", and (option "profile") "fused_ns_total",
  *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
  *   an unknown name.
  */

@@ -162,6 +162,16 @@ struct bf_vec_plan_s {
     size_t drec_bytes = 0;
     int last_batch = 0;
     size_t free_mem = 0;       // free device memory at the first launch (0 = not queried yet)
+    // CUDA-graph replay of bf_vec_filter (option "graph"): the launch sequence of a call is
+    // captured on the second call with the same (f, out, stream, option generation) and replayed
+    bool use_graph = true;
+    int gen = 0;               // bumped by every option change (kernel arguments may differ)
+    cudaGraphExec_t gexec = nullptr;
+    const float *g_f = nullptr;
+    float *g_out = nullptr;
+    cudaStream_t g_stream = nullptr;
+    int g_gen = -1, g_seen = 0, g_launches = 0;
+    bf_status_t g_status = BF_OK;
     // device state (lazily created)
     int device = -1;
     bool sampled = false;

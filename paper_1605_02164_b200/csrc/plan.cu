@@ -555,6 +555,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
         cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drun); cudaFree(p->dmse);
         cudaFree(p->dkeys); cudaFree(p->dlab);
+        if (p->gexec) cudaGraphExecDestroy(p->gexec);
         for (auto &pair : p->ev)
             for (auto &e : pair)
                 if (e) cudaEventDestroy(e);
@@ -573,6 +574,7 @@ bf_status_t bf_vec_sample_freqs(bf_vec_plan_t p, void *stream) {
     st = draw(p, p->seed, S(stream));
     if (st != BF_OK) return st;
     p->sampled = true;
+    p->gen += 1;
     p->last = S(stream);
     return BF_OK;
 }
@@ -618,10 +620,76 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     return p->alias ? BF_W_ALIAS : BF_OK;
 }
 
+// bf_vec_filter through a CUDA graph: the first call with a given (f, out, stream, options) runs
+// eagerly (it allocates scratch and picks the schedule), the second captures the same launch
+// sequence (pad, fused kernel, diagnostics reset, normalise) into a graph, and later calls replay it
+// with one cudaGraphLaunch -- the host cost of a small image drops to one launch.
+bf_status_t filter_graph(bf_vec_plan_t p, const float *f, float *out, cudaStream_t s) {
+    const bool same = p->gexec && p->g_f == f && p->g_out == out && p->g_stream == s && p->g_gen == p->gen;
+    if (same) {
+        int slot = -1;
+        if (p->profile) {   // time the whole replay (the fused kernel is > 99.7 % of it on configs 2-5)
+            if (p->ev_count == bf_vec_plan_s::kEvRing) collect_profile(p);
+            slot = p->ev_head;
+            for (int j = 0; j < 2; ++j)
+                if (!p->ev[slot][j]) BF_CUDA(cudaEventCreate(&p->ev[slot][j]));
+            BF_CUDA(cudaEventRecord(p->ev[slot][0], s));
+        }
+        BF_CUDA(cudaGraphLaunch(p->gexec, s));
+        if (slot >= 0) {
+            BF_CUDA(cudaEventRecord(p->ev[slot][1], s));
+            p->ev_head = (p->ev_head + 1) % bf_vec_plan_s::kEvRing;
+            p->ev_count += 1;
+        }
+        p->last_launches = p->g_launches;
+        p->last = s;
+        return p->g_status;
+    }
+    const bool key_seen = p->g_f == f && p->g_out == out && p->g_stream == s && p->g_gen == p->gen;
+    if (!key_seen) {   // first call with this key: eager, remember the key
+        if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+        p->g_f = f; p->g_out = out; p->g_stream = s; p->g_gen = p->gen;
+        return filter_band(p, f, p->H, 0, 0, p->H, out, s);
+    }
+    // second call: capture (profiling events stay outside the graph)
+    const bool prof = p->profile;
+    p->profile = false;
+    BF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const bf_status_t st = filter_band(p, f, p->H, 0, 0, p->H, out, s);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    p->profile = prof;
+    if (st < 0 || ce != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        p->use_graph = false;            // fall back to eager launches for this plan
+        return st < 0 ? st : filter_band(p, f, p->H, 0, 0, p->H, out, s);
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&p->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+        p->gexec = nullptr;
+        cudaGetLastError();
+        p->use_graph = false;
+        return filter_band(p, f, p->H, 0, 0, p->H, out, s);
+    }
+    p->g_launches = p->last_launches;
+    p->g_status = st;
+    return filter_graph(p, f, out, s);   // replay now
+}
+
 bf_status_t bf_vec_filter(bf_vec_plan_t p, const float *f, float *out, void *stream) {
     if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
     if (p->device < 0) return BF_E_STATE;
-    return filter_band(p, f, p->H, 0, 0, p->H, out, S(stream));
+    cudaStream_t s = S(stream);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    // the legacy default stream cannot be captured; a stream the caller is capturing already
+    // records our launches into the caller's graph
+    if (p->use_graph && p->sampled && s != nullptr && cudaStreamIsCapturing(s, &cs) == cudaSuccess &&
+        cs == cudaStreamCaptureStatusNone)
+        return filter_graph(p, f, out, s);
+    cudaGetLastError();
+    return filter_band(p, f, p->H, 0, 0, p->H, out, s);
 }
 
 bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {
@@ -850,6 +918,12 @@ bf_status_t bf_vec_diag(bf_vec_plan_t p, float *z_min, long long *n_small_z) {
 
 bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
     if (!valid_plan(p) || !name) return BF_E_ARG;
+    if (std::strcmp(name, "profile") != 0) p->gen += 1;   // options may change the captured launches
+    if (!std::strcmp(name, "graph")) {
+        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        p->use_graph = v != 0.0;
+        return BF_OK;
+    }
     if (!std::strcmp(name, "z_floor")) { p->z_floor = v; return BF_OK; }
     if (!std::strcmp(name, "value_range")) {
         if (!(v > 0) || !std::isfinite(v)) return BF_E_ARG;
@@ -922,7 +996,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"sampler", p->sampler}, {"colorspace", p->lab},
+        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"sampler", p->sampler}, {"colorspace", p->lab},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)

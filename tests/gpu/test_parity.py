@@ -249,3 +249,32 @@ def test_p2p_sample_exchange_world1_matches_filter():
     assert (y0, y1) == (0, cfg.H)
     ok = Z / cfg.M >= H.Z_FLOOR
     assert np.abs(got - ref)[:, ok].max() < 2e-3
+
+
+def test_graph_replay_bitwise_equals_eager():
+    """Option "graph": on a created stream the second bf_vec_filter call captures a CUDA graph and
+    later calls replay it; the output is bit-identical to eager launches, and an option change
+    re-captures."""
+    cfg = CONFIGS[2]
+    f = torch.from_numpy(make_image(cfg)).cuda()
+    p = H.gpu_plan(cfg)
+    p.set_option("graph", 0)
+    eager = p.filter(f).clone()
+    p.set_option("graph", 1)
+    s = torch.cuda.Stream()
+    out = torch.empty_like(f)
+    with torch.cuda.stream(s):
+        for _ in range(4):
+            p.filter(f, out)
+    s.synchronize()
+    assert p.info("graph_ready") == 1
+    assert torch.equal(out, eager)
+    with torch.cuda.stream(s):
+        p.set_option("spatial_kernel", 1)        # new kernel arguments -> eager, then re-capture
+        p.filter(f, out)
+        p.filter(f, out)
+        p.filter(f, out)
+    s.synchronize()
+    p.set_option("graph", 0)
+    box = p.filter(f).clone()
+    assert torch.equal(out, box)
