@@ -191,8 +191,11 @@ bf_status_t bf_vec_direct(bf_vec_plan_t plan, const float *f, float *out, void *
  *   f, ref     device planar (d, H, W) float32 (ref: usually bf_vec_direct's output)
  *   seeds      host, n_seeds keys;  t_list  host, n_t strictly increasing values in [1, M]
  *   mse        host, n_seeds x n_t doubles
- * Synchronous on `stream`; restores the plan's own draws before returning. Uses the plan's
- * engine, spatial kernel and sampler options. Errors: BF_E_ARG, BF_E_STATE (sample_freqs
+ * Synchronous on `stream`; the plan's own draws are left as they were. Uses the plan's engine,
+ * spatial kernel and sampler options. With the FIR engine the realisations are batched through
+ * the fused kernel's sample-group dimension (group g = realisation g; as many per batch as 25 %
+ * of the free device memory allows, at most 256): per checkpoint one fused launch and one
+ * reduction kernel serve the whole batch. Errors: BF_E_ARG, BF_E_STATE (sample_freqs
  * not called), BF_E_UNSUPPORTED, BF_E_CUDA.
  */
 bf_status_t bf_vec_mse_sweep(bf_vec_plan_t plan, const float *f, const float *ref, int n_seeds,

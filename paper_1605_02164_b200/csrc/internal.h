@@ -28,6 +28,7 @@ struct alignas(64) FusedArgs {
     int tile_rows;        // rows per CTA tile (multiple of the kernel's KB)
     int groups;           // sample groups (grid.z)
     int k0, k1;           // sample range
+    int gstride;          // 0, or realisation batching: group g filters t rows [g*gstride + k0, g*gstride + k1)
     const float *t;       // (M, d) frequency table, fp32
     float *pz;            // (groups, D+1, out_rows, W): planes 0..D-1 = P' (centred), D = Z
     float w[kMaxR + 1];   // normalised taps w[|m|], zero beyond the plan radius
@@ -119,6 +120,10 @@ struct MuArg {
 };
 cudaError_t launch_mse_accum(const float *pz, int groups, int D, int d, long long npix, const float *mu,
                              float *run, int first, const float *ref, double *out, cudaStream_t s);
+// realisation-batched: group r of pz is realisation r; run holds nr (d+1)-plane running sums;
+// out[r] += sum (ref - S_r)^2
+cudaError_t launch_mse_accum_batch(const float *pz, int nr, int D, int d, long long npix, const float *mu,
+                                   float *run, int first, const float *ref, double *out, cudaStream_t s);
 
 // sRGB <-> CIE-Lab (color.cu; reading R18), planar (3, npix), in place allowed
 cudaError_t launch_srgb_to_lab(const float *in, float *out, long long npix, cudaStream_t s);
@@ -155,6 +160,9 @@ struct bf_vec_plan_s {
     float *dlab = nullptr;     // Lab copy of the input
     size_t dlab_bytes = 0;
     uint64_t *dkeys = nullptr; // stratified sampler: permutation keys (M d)
+    float *dt_batch = nullptr; // error sweep: frequency tables of a batch of realisations
+    int32_t *dX_batch = nullptr;
+    size_t dt_batch_n = 0;
     float *drun = nullptr;     // error sweep: running (P', Z) planes and per-checkpoint sums
     double *dmse = nullptr;
     size_t drun_bytes = 0;

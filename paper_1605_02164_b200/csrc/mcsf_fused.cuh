@@ -205,8 +205,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB) mcsf_fused_kernel(const __grid
     const int ty1 = min(ty0 + a.tile_rows, a.out_row0 + a.out_rows);
     const int g = blockIdx.z;
     const int ns = a.k1 - a.k0;
-    const int gk0 = a.k0 + (int)((long long)ns * g / a.groups);
-    const int gk1 = a.k0 + (int)((long long)ns * (g + 1) / a.groups);
+    // sample range of group g: a slice of [k0, k1), or -- realisation batching (gstride > 0,
+    // bf_vec_mse_sweep) -- the same [k0, k1) of realisation g's draws at t rows g * gstride + k
+    const int gk0 = a.gstride ? a.k0 + g * a.gstride : a.k0 + (int)((long long)ns * g / a.groups);
+    const int gk1 = a.gstride ? a.k1 + g * a.gstride : a.k0 + (int)((long long)ns * (g + 1) / a.groups);
     const int nchunks = (ty1 - ty0 + C::KB - 1) / C::KB;
     const int rows_per_sample = nchunks * C::KB + 2 * C::R;
     // padded-copy row of tile-frame row u = 0 (image row ty0 - R): pad row 0 is image row out_row0 - R

@@ -145,8 +145,10 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem_kernel(const __grid_consta
     const int ty1 = min(ty0 + a.tile_rows, a.out_row0 + a.out_rows);
     const int g = blockIdx.z;
     const int ns = a.k1 - a.k0;
-    const int gk0 = a.k0 + (int)((long long)ns * g / a.groups);
-    const int gk1 = a.k0 + (int)((long long)ns * (g + 1) / a.groups);
+    // sample range of group g: a slice of [k0, k1), or -- realisation batching (gstride > 0,
+    // bf_vec_mse_sweep) -- the same [k0, k1) of realisation g's draws at t rows g * gstride + k
+    const int gk0 = a.gstride ? a.k0 + g * a.gstride : a.k0 + (int)((long long)ns * g / a.groups);
+    const int gk1 = a.gstride ? a.k1 + g * a.gstride : a.k0 + (int)((long long)ns * (g + 1) / a.groups);
     const int nchunks = (ty1 - ty0 + C::KB - 1) / C::KB;
     const int rows_per_sample = C::A + (nchunks - 1) * C::KB;   // multiple of 16
     const int prow0 = ty0 - a.out_row0;

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "internal.h"
 
@@ -284,12 +285,21 @@ struct P2POut {
     int world, rank, slots;
 };
 
+// realisation batching for bf_vec_mse_sweep: group g filters samples [k0, k1) of realisation g,
+// whose draws are rows [g * stride, (g + 1) * stride) of the table t
+struct RealBatch {
+    const float *t;
+    int groups, stride;
+};
+
 bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_row0, int out_row0,
-                      int out_rows, int k0, int k1, cudaStream_t s, int *groups_out, const P2POut *p2p = nullptr) {
+                      int out_rows, int k0, int k1, cudaStream_t s, int *groups_out, const P2POut *p2p = nullptr,
+                      const RealBatch *rb = nullptr) {
     if (!p->kinfo_ok) return BF_E_UNSUPPORTED;   // r > 64 or no compiled instance: engine 1 only
     int tile_rows = 0, groups = 1;
     choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups);
     if (p2p) groups = p2p->slots;   // one receive slot per (rank, group) on every owner
+    if (rb) groups = rb->groups;    // one realisation per group
     const KernelInfo &ki = p->kinfo;
     const size_t need = sizeof(float) * (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;
     bf_status_t st = ensure_pz(p, need);
@@ -320,7 +330,8 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
     a.groups = groups;
     a.k0 = k0;
     a.k1 = k1;
-    a.t = p->dt;
+    a.t = rb ? rb->t : p->dt;
+    a.gstride = rb ? rb->stride : 0;
     a.pz = p->dpz;
     for (int i = 0; i <= kMaxR; ++i) a.w[i] = (i <= p->r) ? p->taps[i] : 0.f;
     if (p2p) {
@@ -554,7 +565,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
         cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drun); cudaFree(p->dmse);
-        cudaFree(p->dkeys); cudaFree(p->dlab);
+        cudaFree(p->dkeys); cudaFree(p->dlab); cudaFree(p->dt_batch); cudaFree(p->dX_batch);
         if (p->gexec) cudaGraphExecDestroy(p->gexec);
         for (auto &pair : p->ev)
             for (auto &e : pair)
@@ -860,6 +871,71 @@ bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, 
         p->dmse_n = n_t;
     }
     bf_status_t st = BF_OK;
+    if (p->engine == 0) {
+        // realisations batched through the fused kernel's group dimension: per checkpoint ONE fused
+        // launch filters the new samples of every realisation of the batch, and one kernel folds
+        // them into each realisation's running sums and reduces its squared error
+        const int D = p->kinfo.D;
+        const double per = 4.0 * npix * ((D + 1) + (p->d + 1));
+        int RB = (int)std::max(1.0, std::min<double>(256.0, 0.25 * (double)free_memory(p) / per));
+        RB = std::min(RB, n_seeds);
+        const size_t tn = (size_t)RB * p->M * p->d;
+        if (p->dt_batch_n < tn) {
+            cudaFree(p->dt_batch); cudaFree(p->dX_batch);
+            p->dt_batch = nullptr; p->dX_batch = nullptr; p->dt_batch_n = 0;
+            BF_CUDA(cudaMalloc(&p->dt_batch, sizeof(float) * tn));
+            BF_CUDA(cudaMalloc(&p->dX_batch, sizeof(int32_t) * tn));
+            p->dt_batch_n = tn;
+        }
+        const size_t rb_bytes = sizeof(float) * (size_t)RB * (p->d + 1) * npix;
+        if (p->drun_bytes < rb_bytes) {
+            cudaFree(p->drun);
+            p->drun = nullptr; p->drun_bytes = 0;
+            BF_CUDA(cudaMalloc(&p->drun, rb_bytes));
+            p->drun_bytes = rb_bytes;
+        }
+        if (p->dmse_n < RB * n_t) {
+            cudaFree(p->dmse);
+            p->dmse = nullptr; p->dmse_n = 0;
+            BF_CUDA(cudaMalloc(&p->dmse, sizeof(double) * RB * n_t));
+            p->dmse_n = RB * n_t;
+        }
+        std::vector<double> host((size_t)RB * n_t);
+        for (int r0 = 0; r0 < n_seeds && st == BF_OK; r0 += RB) {
+            const int nr = std::min(RB, n_seeds - r0);
+            for (int r = 0; r < nr; ++r) {
+                const size_t off = (size_t)r * p->M * p->d;
+                if (p->sampler == 1) {
+                    if (!p->dkeys) BF_CUDA(cudaMalloc(&p->dkeys, sizeof(uint64_t) * (size_t)p->M * p->d));
+                    BF_CUDA(launch_sampler_stratified(p->M, p->d, p->N, seeds[r0 + r], p->dQ, p->dgamma, p->dkeys,
+                                                      p->dX_batch + off, p->dt_batch + off, s));
+                } else {
+                    BF_CUDA(launch_sampler(p->M, p->d, p->N, seeds[r0 + r], p->dQ, p->dgamma, p->dX_batch + off,
+                                           p->dt_batch + off, s));
+                }
+            }
+            BF_CUDA(cudaMemsetAsync(p->dmse, 0, sizeof(double) * nr * n_t, s));
+            int k0 = 0;
+            for (int j = 0; j < n_t && st == BF_OK; ++j) {
+                const RealBatch rbatch{p->dt_batch, nr, p->M};
+                int groups = 1;
+                st = run_fused(p, f, p->H, 0, 0, p->H, k0, t_list[j], s, &groups, nullptr, &rbatch);
+                if (st != BF_OK) break;
+                BF_CUDA(launch_mse_accum_batch(p->dpz, nr, D, p->d, npix, p->mu, p->drun, j == 0 ? 1 : 0, ref,
+                                               p->dmse + (size_t)j * nr, s));
+                k0 = t_list[j];
+            }
+            if (st != BF_OK) break;
+            BF_CUDA(cudaMemcpyAsync(host.data(), p->dmse, sizeof(double) * nr * n_t, cudaMemcpyDeviceToHost, s));
+            BF_CUDA(cudaStreamSynchronize(s));
+            for (int r = 0; r < nr; ++r)
+                for (int j = 0; j < n_t; ++j)
+                    mse[(size_t)(r0 + r) * n_t + j] = host[(size_t)j * nr + r] / ((double)p->d * (double)npix);
+        }
+        p->last = s;
+        p->last_launches = 0;
+        return st;
+    }
     for (int r = 0; r < n_seeds && st == BF_OK; ++r) {
         // realisation r: the same generator keyed by seeds[r] (reading R9)
         st = draw(p, seeds[r], s);

@@ -42,7 +42,50 @@ __global__ void mse_accum_kernel(const float *__restrict__ pz, int groups, int D
     }
 }
 
+// one (pixel block, realisation) per CTA: fold realisation r's partial planes into its running sums,
+// S_r = P'_r / Z_r + mu, and add sum_c (ref - S_r)^2 to out[r]
+__global__ void mse_accum_batch_kernel(const float *__restrict__ pz, int D, int d, long long npix, MuArg mu,
+                                       float *__restrict__ run, int first, const float *__restrict__ ref,
+                                       double *__restrict__ out) {
+    const int r = blockIdx.y;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const float *pr = pz + (long long)r * (D + 1) * npix;
+    float *rr = run + (long long)r * (d + 1) * npix;
+    double err = 0.0;
+    if (e < npix) {
+        const float z = (first ? 0.f : rr[(long long)d * npix + e]) + pr[(long long)D * npix + e];
+        rr[(long long)d * npix + e] = z;
+        const float rz = 1.0f / z;
+        for (int c = 0; c < d; ++c) {
+            const float p = (first ? 0.f : rr[(long long)c * npix + e]) + pr[(long long)c * npix + e];
+            rr[(long long)c * npix + e] = p;
+            const double diff = (double)ref[(long long)c * npix + e] - (double)(p * rz + mu.v[c]);
+            err += diff * diff;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) err += __shfl_xor_sync(0xffffffffu, err, o);
+    __shared__ double part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = err;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += part[i];
+        atomicAdd(out + r, s);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_mse_accum_batch(const float *pz, int nr, int D, int d, long long npix, const float *mu,
+                                   float *run, int first, const float *ref, double *out, cudaStream_t s) {
+    MuArg m;
+    for (int c = 0; c < kMaxD; ++c) m.v[c] = mu[c];
+    const int threads = 256;
+    dim3 grid((unsigned)((npix + threads - 1) / threads), (unsigned)nr);
+    mse_accum_batch_kernel<<<grid, threads, 0, s>>>(pz, D, d, npix, m, run, first, ref, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_mse_accum(const float *pz, int groups, int D, int d, long long npix, const float *mu,
                              float *run, int first, const float *ref, double *out, cudaStream_t s) {
