@@ -234,8 +234,9 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 memory double ring, two samples per pass, two consumer warps per pair,
  *                 four dedicated modulation warps (d <= 3, r in (10, 48]), 5 v5 with one
  *                 consumer warp per pair, 6 v5c (v6 without the modulation warps) (both
- *                 d = 3, r in (30, 48]); a variant not compiled for the plan falls back to the
- *                 default order
+ *                 d = 3, r in (30, 48]), 7 v6 with running-sum FIRs for box taps (d = 3,
+ *                 spatial_kernel = 1, r in {15, 24, 30, 48}; chosen automatically for box
+ *                 taps); a variant not compiled for the plan falls back to the default order
  *   "engine"      how Alg. 1 step 10 convolves: 0 (default) the truncated
  *                 separable window [-r, r] of Eq. (1) / "spatial_kernel", O(r) per pixel-sample
  *                 (fused sm_100a kernel); 1 the recursive O(1)-in-sigma_s engine of PAPER.md:204

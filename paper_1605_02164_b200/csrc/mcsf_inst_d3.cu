@@ -41,6 +41,12 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
             return true;
         }
     }
+    if (variant == 7) {   // box taps with the window exactly R: running-sum FIRs (option spatial_kernel = 1)
+#define BFV_FILLB(D_, R_) \
+    if (R_ == r) { fill_info_tmem2<CfgT2<D_, R_, 2, 4, true>>(info); info->variant = 7; return true; }
+        BFV_TMEM2_INSTANCES(BFV_FILLB)
+#undef BFV_FILLB
+    }
     if (variant == 6 && bestT == 48) {   // v5c: modulation by the producer warps (comparison instance)
         fill_info_tmem2<CfgT2<3, 48, 2, 0>>(info);
         info->variant = 6;
@@ -77,6 +83,13 @@ cudaError_t fused_launch_d3(const KernelInfo &info, const FusedArgs &a, dim3 gri
     if (info.variant == 3) return launch_tmem<CfgT<3, 48, 16, 2>>(a, grid, s);
     if (info.variant == 5) return launch_tmem2<CfgT2<3, 48, 1>>(a, grid, s);
     if (info.variant == 6) return launch_tmem2<CfgT2<3, 48, 2, 0>>(a, grid, s);
+    if (info.variant == 7) {
+#define BFV_LAUNCHB(D_, R_) \
+    if (info.R == R_) return launch_tmem2<CfgT2<D_, R_, 2, 4, true>>(a, grid, s);
+        BFV_TMEM2_INSTANCES(BFV_LAUNCHB)
+#undef BFV_LAUNCHB
+        return cudaErrorInvalidValue;
+    }
     if (info.variant == 4) {
 #define BFV_LAUNCH2(D_, R_) \
     if (info.R == R_) return launch_tmem2<CfgT2<D_, R_, 2, 4>>(a, grid, s);

@@ -21,7 +21,7 @@
 namespace bfvec {
 namespace {
 
-template <int D_, int R_, int CW_ = 1, int MW_ = 0>
+template <int D_, int R_, int CW_ = 1, int MW_ = 0, bool BOX_ = false>
 struct CfgT2 {
     static constexpr int D = D_;
     static constexpr int R = R_;
@@ -35,6 +35,7 @@ struct CfgT2 {
     static constexpr int OR = KB / CW_;      //   output rows OR (w >> 2) .. + OR of every chunk
     static constexpr int NB = 128 * CW_;
     static constexpr int MW = MW_;           // dedicated modulation warps (0: the producers modulate)
+    static constexpr bool BOX = BOX_;        // box taps (all equal, window exactly R): running sums
     static constexpr int NM = 32 * MW_;
     static constexpr int NT = NA + NB + NM;
     static constexpr int DP = 4;
@@ -86,6 +87,32 @@ __device__ __forceinline__ void tmem_wait_rows(float2 (&v)[LR]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < LR; ++i) asm volatile("" : "+f"(v[i].x), "+f"(v[i].y));
+}
+
+// One FIR input v = x[J] (J = compile-time index into the item's input window) for NOUT consecutive
+// outputs: out[o] = sum_{m=-R..R} w[|m|] x[o + R + m].
+//  * general taps: every output the input reaches gets one FFMA2;
+//  * box taps (BOX, "box ... filter", reading R15; all weights w = 1/(2R+1)): a running
+//    sum -- out[0] takes x[0..2R], then out[o] = out[o-1] + w x[o+2R] - w x[o-1] -- so NOUT outputs
+//    cost 2R+1 + 2(NOUT-1) FFMA2 instead of NOUT (2R+1); x[0..NOUT-2] are kept for the subtraction.
+template <class C, int NOUT, int J>
+__device__ __forceinline__ void fir_input(const FusedArgs &a, float2 (&acc)[NOUT], float2 (&early)[NOUT], float2 v) {
+    if constexpr (C::BOX) {
+        const float w = a.w[0];
+        if constexpr (J <= 2 * C::R) acc[0] = ffma2(w, v, acc[0]);
+        if constexpr (J < NOUT - 1) early[J] = v;
+        if constexpr (J > 2 * C::R && J - 2 * C::R < NOUT) {
+            constexpr int o = J - 2 * C::R;
+            acc[o] = ffma2(-w, early[o - 1], ffma2(w, v, acc[o - 1]));
+        }
+    } else {
+        (void)early;
+        static_for<NOUT>([&](auto O) {
+            constexpr int o = decltype(O)::value;
+            constexpr int m = J - o - C::R;
+            if constexpr (m >= -C::R && m <= C::R) acc[o] = ffma2(a.w[m < 0 ? -m : m], v, acc[o]);
+        });
+    }
 }
 
 // modulation of one SH-row sub-step for the pass's samples (np of them) into G[buf][s]
@@ -228,23 +255,14 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                         if (p < C::NP && sw < np) {
                             // horizontal FIR: 8 outputs (row r8, columns 8cg .. 8cg+7) of sample sw
                             const float2 *in = (sw == 0 ? gb0 : gb1) + (p * C::SH + r8) * C::MS + cg * 8;
-                            float2 acc[8];
+                            float2 acc[8], early[8];
 #pragma unroll
                             for (int o = 0; o < 8; ++o) acc[o] = make_float2(0.f, 0.f);
                             static_for<C::NIN / 2>([&](auto JJ) {
                                 constexpr int jj = decltype(JJ)::value;
                                 const float4 v2 = *reinterpret_cast<const float4 *>(in + 2 * jj);
-                                const float2 v[2] = {make_float2(v2.x, v2.y), make_float2(v2.z, v2.w)};
-                                static_for<2>([&](auto E) {
-                                    constexpr int e = decltype(E)::value;
-                                    constexpr int j = 2 * jj + e;
-                                    static_for<8>([&](auto O) {
-                                        constexpr int o = decltype(O)::value;
-                                        constexpr int m = j - o - C::R;
-                                        if constexpr (m >= -C::R && m <= C::R)
-                                            acc[o] = ffma2(a.w[m < 0 ? -m : m], v[e], acc[o]);
-                                    });
-                                });
+                                fir_input<C, 8, 2 * jj>(a, acc, early, make_float2(v2.x, v2.y));
+                                fir_input<C, 8, 2 * jj + 1>(a, acc, early, make_float2(v2.z, v2.w));
                             });
                             if constexpr (C::MW > 0) mbar_arrive(&gempty[buf]);   // G[buf] read
                             // transpose through this warp's shared-memory tile: lane (r8, cg) holds
@@ -351,7 +369,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
 #pragma unroll 1
                     for (int s = 0; s < np; ++s) {
                         const uint32_t tr = tq + (uint32_t)(s * C::RCOLS);
-                        float2 acc[OR];
+                        float2 acc[OR], early[OR];
 #pragma unroll
                         for (int o = 0; o < OR; ++o) acc[o] = make_float2(0.f, 0.f);
                         float2 v[2][LR];
@@ -366,12 +384,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                             if constexpr (bj + 1 < JB1) tmem_ld_rows<LR>(tr + 2 * slot_of(bj + 1), v[(bj + 1) & 1]);
                             static_for<LR>([&](auto JJ) {
                                 constexpr int j = LR * bj + decltype(JJ)::value;
-                                static_for<OR>([&](auto O) {
-                                    constexpr int o = decltype(O)::value;
-                                    constexpr int m = j - o - C::R;
-                                    if constexpr (m >= -C::R && m <= C::R)
-                                        acc[o] = ffma2(a.w[m < 0 ? -m : m], v[bj & 1][decltype(JJ)::value], acc[o]);
-                                });
+                                fir_input<C, OR, j>(a, acc, early, v[bj & 1][decltype(JJ)::value]);
                             });
                             if constexpr (bj + 1 < JB1) tmem_wait_rows<LR>(v[(bj + 1) & 1]);
                         });

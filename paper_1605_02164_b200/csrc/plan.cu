@@ -118,6 +118,20 @@ bf_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? BF_OK : BF_E_
         if (_e != cudaSuccess) return BF_E_CUDA;             \
     } while (0)
 
+// Kernel instance for the plan: the forced variant, else -- box taps whose window is a compiled
+// radius -- the running-sum instance (variant 7), else the default order (fused_select).
+bool select_kernel(bf_vec_plan_t p) {
+    if (p->r > kMaxR) return false;
+    if (p->force_variant == 0 && p->spatial == 1) {
+        bfvec::KernelInfo ki;
+        if (fused_select(p->d, p->r, 7, &ki) && ki.variant == 7) {
+            p->kinfo = ki;
+            return true;
+        }
+    }
+    return fused_select(p->d, p->r, p->force_variant, &p->kinfo);
+}
+
 bf_status_t ensure_device(bf_vec_plan_t p) {
     if (p->device >= 0) return BF_OK;
     int dev = 0;
@@ -130,7 +144,7 @@ bf_status_t ensure_device(bf_vec_plan_t p) {
     BF_CUDA(cudaMalloc(&p->dQ, sizeof(double) * 64));
     BF_CUDA(cudaMalloc(&p->dgamma, sizeof(double) * 8));
     BF_CUDA(cudaMalloc(&p->ddiag, 16));
-    p->kinfo_ok = p->r <= kMaxR && fused_select(p->d, p->r, p->force_variant, &p->kinfo);
+    p->kinfo_ok = select_kernel(p);
     p->device = dev;
     return BF_OK;
 }
@@ -1016,12 +1030,11 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
     if (!std::strcmp(name, "tile_rows")) { if (v < 0) return BF_E_ARG; p->force_tile_rows = (int)v; return BF_OK; }
     if (!std::strcmp(name, "groups")) { if (v < 0) return BF_E_ARG; p->force_groups = (int)v; return BF_OK; }
     if (!std::strcmp(name, "variant")) {
-        if (v < 0 || v > 6) return BF_E_ARG;
+        if (v < 0 || v > 7) return BF_E_ARG;
         p->force_variant = (int)v;
         if (p->device >= 0) {   // re-select the kernel instance
-            bfvec::KernelInfo ki;
-            if (!fused_select(p->d, p->r, p->force_variant, &ki)) return BF_E_UNSUPPORTED;
-            p->kinfo = ki;
+            if (!select_kernel(p)) return BF_E_UNSUPPORTED;
+            p->kinfo_ok = true;
         }
         return BF_OK;
     }
@@ -1046,6 +1059,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
         p->spatial = (int)v;
         make_taps(p);
+        if (p->device >= 0) p->kinfo_ok = select_kernel(p);   // box: running-sum instance
         return BF_OK;
     }
     if (!std::strcmp(name, "profile")) {
