@@ -106,6 +106,16 @@ bf_status_t bf_vec_get_draws(bf_vec_plan_t plan, int32_t *X, float *t, double *Q
 bf_status_t bf_vec_filter(bf_vec_plan_t plan, const float *f, float *out, void *stream);
 
 /*
+ * bf_vec_filter_batch -- bf_vec_filter for nimg images of the plan's size in ONE fused launch
+ * (the images are independent units): the grid covers every image's strips, so small
+ * images fill the GPU. Every image uses the plan's draws (as nimg bf_vec_filter calls would).
+ *   f, out   device planar (nimg, d, H, W) float32, contiguous; out may not alias f
+ * FIR engine only and no colorspace (else BF_E_UNSUPPORTED); BF_W_ALIAS as bf_vec_filter;
+ * bf_vec_diag reports the small-Z statistics over all images.
+ */
+bf_status_t bf_vec_filter_batch(bf_vec_plan_t plan, const float *f, float *out, int nimg, void *stream);
+
+/*
  * bf_vec_filter_host -- bf_vec_filter on HOST buffers: copies f (d,H,W) to the
  * device, filters, copies out back, and synchronises `stream`. Pinned host
  * memory gives full PCIe bandwidth; pageable memory works but is slower.

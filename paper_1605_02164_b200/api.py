@@ -109,6 +109,16 @@ class Plan:
                                                          _stream_ptr(stream)), "bf_vec_filter")
         return out
 
+    def filter_batch(self, f, out=None, stream=None):
+        """bf_vec_filter_batch: f (nimg, d, H, W) device tensor -> (nimg, d, H, W)."""
+        nimg = f.shape[0]
+        shp = (nimg, self.d, self.H, self.W)
+        if out is None:
+            out = torch.empty(shp, dtype=torch.float32, device=f.device)
+        self.last_status = check(self._lib.bf_vec_filter_batch(self._h, _dev(f, shp, "f"), _dev(out, shp, "out"),
+                                                               int(nimg), _stream_ptr(stream)), "bf_vec_filter_batch")
+        return out
+
     def filter_host(self, f_host, out_host=None, stream=None):
         """bf_vec_filter_host: host (pinned) tensors in and out; synchronous."""
         shp = (self.d, self.H, self.W)

@@ -29,6 +29,10 @@ struct alignas(64) FusedArgs {
     int groups;           // sample groups (grid.z)
     int k0, k1;           // sample range
     int gstride;          // 0, or realisation batching: group g filters t rows [g*gstride + k0, g*gstride + k1)
+    // image batching (bf_vec_filter_batch): blockIdx.y = image * tiles_per_img + tile; image i's padded
+    // rows start at i * img_prows in the tensor map and its partial planes at pz + i * img_pz
+    int tiles_per_img, img_prows;
+    long long img_pz;
     const float *t;       // (M, d) frequency table, fp32
     float *pz;            // (groups, D+1, out_rows, W): planes 0..D-1 = P' (centred), D = Z
     float w[kMaxR + 1];   // normalised taps w[|m|], zero beyond the plan radius

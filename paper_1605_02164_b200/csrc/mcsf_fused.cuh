@@ -201,7 +201,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) mcsf_fused_kernel(const __grid
 
     const int tid = threadIdx.x;
     const int x0 = blockIdx.x * C::TX;
-    const int ty0 = a.out_row0 + blockIdx.y * a.tile_rows;
+    const int img = a.tiles_per_img ? (int)blockIdx.y / a.tiles_per_img : 0;     // image of the batch
+    const int tile = a.tiles_per_img ? (int)blockIdx.y % a.tiles_per_img : (int)blockIdx.y;
+    const int ty0 = a.out_row0 + tile * a.tile_rows;
     const int ty1 = min(ty0 + a.tile_rows, a.out_row0 + a.out_rows);
     const int g = blockIdx.z;
     const int ns = a.k1 - a.k0;
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) mcsf_fused_kernel(const __grid
     const int nchunks = (ty1 - ty0 + C::KB - 1) / C::KB;
     const int rows_per_sample = nchunks * C::KB + 2 * C::R;
     // padded-copy row of tile-frame row u = 0 (image row ty0 - R): pad row 0 is image row out_row0 - R
-    const int prow0 = ty0 - a.out_row0;
+    const int prow0 = img * a.img_prows + (ty0 - a.out_row0);
 
     if (tid == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tmap)) : "memory");
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) mcsf_fused_kernel(const __grid
         const bool xok = x < a.W;
         const long long plane_out = (long long)a.out_rows * a.W;
         const int plane = (p == 0) ? C::D : p - 1;
-        float *pzp = a.pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
+        float *pzp = a.pz + img * a.img_pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
         int q = 0;
         for (int k = gk0; k < gk1; ++k) {
             const bool first_k = (k == gk0);

@@ -215,7 +215,9 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int x0 = blockIdx.x * C::TX;
-    const int ty0 = a.out_row0 + blockIdx.y * a.tile_rows;
+    const int img = a.tiles_per_img ? (int)blockIdx.y / a.tiles_per_img : 0;     // image of the batch
+    const int tile = a.tiles_per_img ? (int)blockIdx.y % a.tiles_per_img : (int)blockIdx.y;
+    const int ty0 = a.out_row0 + tile * a.tile_rows;
     const int ty1 = min(ty0 + a.tile_rows, a.out_row0 + a.out_rows);
     const int g = blockIdx.z;
     const int ns = a.k1 - a.k0;
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
     const int gk1 = a.gstride ? a.k1 + g * a.gstride : a.k0 + (int)((long long)ns * (g + 1) / a.groups);
     const int nchunks = (ty1 - ty0 + C::KB - 1) / C::KB;
     const int rows_per_pass = C::A + (nchunks - 1) * C::KB;   // multiple of 16
-    const int prow0 = ty0 - a.out_row0;
+    const int prow0 = img * a.img_prows + (ty0 - a.out_row0);
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(taddr_s)),
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
             const bool xok = x < a.W;
             const long long plane_out = (long long)a.out_rows * a.W;
             const int plane = (p == 0) ? C::D : p - 1;
-            float *pzp = a.pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
+            float *pzp = a.pz + img * a.img_pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
             constexpr int OR = C::OR;
             constexpr int LR = (OR == 16) ? 16 : 8;                  // ring rows per TMEM load
             constexpr int JB1 = (OR - 1 + 2 * C::R) / LR + 1;        // loads per window

@@ -179,7 +179,7 @@ size_t free_memory(bf_vec_plan_t p) {
 // Choose (tile_rows, groups) for one fused launch by a simple cost model:
 // per CTA time ~ samples x (H-pass rows + V-pass rows + per-chunk overhead),
 // whole launch ~ waves x CTA time + the partial-sum traffic of G groups.
-void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows, int *groups) {
+void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows, int *groups, int nimg = 1) {
     const KernelInfo &ki = p->kinfo;
     const int KB = ki.kb, R = ki.R, D = ki.D;
     const int nx = (p->W + kTX - 1) / kTX;
@@ -198,8 +198,8 @@ void choose_schedule(const bf_vec_plan_t p, int out_rows, int ns, int *tile_rows
         const int ny = (out_rows + t - 1) / t;
         const int chunks = (std::min(t, out_rows) + KB - 1) / KB;
         for (int G = 1; G <= std::min(ns, 256); ++G) {
-            const long long ctas = (long long)nx * ny * G;
-            if (ctas > 2147483647LL / 2 || (long long)ny > 65535) continue;
+            const long long ctas = (long long)nx * ny * G * nimg;
+            if (ctas > 2147483647LL / 2 || (long long)ny * nimg > 65535) continue;
             // partial sums: G x (D+1) planes; keep them within a quarter of the free memory
             // (at most 24 GiB), or 4 groups, whichever is larger
             const double pz_bytes = (double)G * (D + 1) * out_rows * (double)p->W * 4.0;
@@ -308,20 +308,20 @@ struct RealBatch {
 
 bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_row0, int out_row0,
                       int out_rows, int k0, int k1, cudaStream_t s, int *groups_out, const P2POut *p2p = nullptr,
-                      const RealBatch *rb = nullptr) {
+                      const RealBatch *rb = nullptr, int nimg = 1) {
     if (!p->kinfo_ok) return BF_E_UNSUPPORTED;   // r > 64 or no compiled instance: engine 1 only
     int tile_rows = 0, groups = 1;
-    choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups);
+    choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups, nimg);
     if (p2p) groups = p2p->slots;   // one receive slot per (rank, group) on every owner
     if (rb) groups = rb->groups;    // one realisation per group
     const KernelInfo &ki = p->kinfo;
-    const size_t need = sizeof(float) * (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;
-    bf_status_t st = ensure_pz(p, need);
+    const size_t img_pz = (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;   // partial floats per image
+    bf_status_t st = ensure_pz(p, sizeof(float) * img_pz * nimg);
     if (st != BF_OK) return st;
     // reflect-padded, centred, interleaved copy of the rows this launch reads (pad.cu)
     const int R = ki.R;
     const int Hp = out_rows + 2 * R, Wp = p->W + 2 * R;
-    const size_t fbytes = sizeof(float) * (size_t)Hp * Wp * ki.dp;
+    const size_t fbytes = sizeof(float) * (size_t)Hp * Wp * ki.dp * nimg;
     if (p->fpad_bytes < fbytes) {
         cudaFree(p->dfpad);
         p->dfpad = nullptr;
@@ -330,11 +330,13 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
         p->fpad_bytes = fbytes;
     }
     fill_mu(p);
-    BF_CUDA(launch_pad(f, (long long)slab_rows * p->W, p->d, p->H, p->W, slab_row0, slab_rows, out_row0 - R, Hp, Wp,
-                       R, ki.dp, p->mu, p->dfpad, s));
+    for (int b = 0; b < nimg; ++b)   // image b of a batch: input at b * d * slab_rows * W, padded block b
+        BF_CUDA(launch_pad(f + (size_t)b * p->d * slab_rows * p->W, (long long)slab_rows * p->W, p->d, p->H, p->W,
+                           slab_row0, slab_rows, out_row0 - R, Hp, Wp, R, ki.dp, p->mu,
+                           p->dfpad + (size_t)b * Hp * Wp * ki.dp, s));
     FusedArgs a;
     std::memset(&a, 0, sizeof(a));
-    st = encode_tmap(&a.tmap, p->dfpad, ki.dp, Wp, Hp, ki.win, ki.sh);
+    st = encode_tmap(&a.tmap, p->dfpad, ki.dp, Wp, Hp * nimg, ki.win, ki.sh);
     if (st != BF_OK) return st;
     a.d = p->d;
     a.W = p->W;
@@ -354,7 +356,13 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
         a.p2p_rank = p2p->rank;
         a.p2p_rpb = p->H / p2p->world;
     }
-    dim3 grid((p->W + kTX - 1) / kTX, (out_rows + tile_rows - 1) / tile_rows, groups);
+    const int ny = (out_rows + tile_rows - 1) / tile_rows;
+    if (nimg > 1) {
+        a.tiles_per_img = ny;
+        a.img_prows = Hp;
+        a.img_pz = (long long)img_pz;
+    }
+    dim3 grid((p->W + kTX - 1) / kTX, ny * nimg, groups);
     p->last_tile_rows = tile_rows;
     p->last_groups = groups;
     p->last_ctas = (long long)grid.x * grid.y * grid.z;
@@ -715,6 +723,26 @@ bf_status_t bf_vec_filter(bf_vec_plan_t p, const float *f, float *out, void *str
         return filter_graph(p, f, out, s);
     cudaGetLastError();
     return filter_band(p, f, p->H, 0, 0, p->H, out, s);
+}
+
+bf_status_t bf_vec_filter_batch(bf_vec_plan_t p, const float *f, float *out, int nimg, void *stream) {
+    if (!valid_plan(p) || !f || !out || f == out || nimg < 1) return BF_E_ARG;
+    if (p->device < 0 || !p->sampled) return BF_E_STATE;
+    if (p->engine != 0 || p->lab) return BF_E_UNSUPPORTED;
+    if ((long long)((p->H + 15) / 16) * nimg > 65535) return BF_E_UNSUPPORTED;   // grid.y
+    cudaStream_t s = S(stream);
+    int groups = 1;
+    bf_status_t st = run_fused(p, f, p->H, 0, 0, p->H, 0, p->M, s, &groups, nullptr, nullptr, nimg);
+    if (st != BF_OK) return st;
+    const size_t img_pz = (size_t)groups * (p->kinfo.D + 1) * p->H * (size_t)p->W;
+    BF_CUDA(launch_diag_reset(p->ddiag, s));
+    for (int b = 0; b < nimg; ++b)
+        BF_CUDA(launch_normalize_groups(p->dpz + b * img_pz, groups, p->kinfo.D, p->d, p->H, p->W, p->mu,
+                                        out + (size_t)b * p->d * p->H * p->W, p->ddiag, 1.0f / p->M,
+                                        (float)p->z_floor, s));
+    p->last_launches = 2 * nimg + 2;
+    p->last = s;
+    return p->alias ? BF_W_ALIAS : BF_OK;
 }
 
 bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {

@@ -278,3 +278,23 @@ def test_graph_replay_bitwise_equals_eager():
     p.set_option("graph", 0)
     box = p.filter(f).clone()
     assert torch.equal(out, box)
+
+
+@pytest.mark.parametrize("case", [(3, 64, 64, 3, 2.0, 20, 32), (5, 37, 45, 3, 5.0, 30, 9), (2, 96, 64, 8, 3.0, 20, 6),
+                                  (4, 40, 33, 1, 16.0, 40, 5)])
+def test_filter_batch_matches_single_images(case):
+    """bf_vec_filter_batch (one fused launch over all images) equals per-image filtering up to the
+    fp32 summation order of the sample groups, and each image matches the oracle."""
+    nimg, Hh, W, d, s, N, M = case
+    cfg = _edge_cfg((Hh, W, d, s, N, M, 40 + nimg, "diag"))
+    imgs = np.stack([random_image(Hh, W, d, seed=100 + i, smooth=bool(i % 2)) for i in range(nimg)])
+    p = H.gpu_plan(cfg)
+    fb = torch.from_numpy(imgs).cuda()
+    batch = p.filter_batch(fb).cpu().numpy()
+    Q, a, Y = H.oracle_draws(cfg)
+    for i in range(nimg):
+        single = p.filter(torch.from_numpy(imgs[i]).cuda()).cpu().numpy()
+        S_o, P_o, Z_o = native.mcsf_full(imgs[i], Q, a, N, Y, s)
+        ok = Z_o / M >= H.Z_FLOOR
+        assert np.abs(batch[i] - single)[:, ok].max() < 2e-3, i
+        assert np.abs(batch[i] - S_o)[:, ok].max() <= H.GATE_B * cfg.value_range / 255.0, i
