@@ -9,7 +9,7 @@
 namespace bfvec {
 
 #define BFV_INSTANCES(X) X(2, 6, 96, 16, 16) X(2, 15, 96, 16, 16) X(2, 32, 96, 16, 16) X(2, 64, 96, 16, 8)
-#define BFV_TMEM2_INSTANCES(X) X(2, 15) X(2, 24) X(2, 30) X(2, 48)
+#define BFV_TMEM2_INSTANCES(X) X(2, 6) X(2, 10) X(2, 15) X(2, 24) X(2, 30) X(2, 48)
 #define BFV_TMEM_INSTANCES(X) X(2, 6) X(2, 15) X(2, 24) X(2, 32) X(2, 48)
 
 // variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 4 force v5
