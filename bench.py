@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 = library default)")
     ap.add_argument("--engine", type=int, default=0, help="0 truncated FIR (default), 1 recursive O(1) engine")
     ap.add_argument("--sigma", type=float, default=0.0, help="override the config's sigma_s (engine sweeps)")
+    ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled (default)")
     return ap.parse_args()
 
 
@@ -253,6 +254,8 @@ def run_ours(args, cfg):
         plan.set_option("variant", args.variant)
     if args.engine:
         plan.set_option("engine", args.engine)
+    if args.rec_impl >= 0:
+        plan.set_option("rec_impl", args.rec_impl)
     plan.sample_freqs()
 
     # this rank's work

@@ -267,9 +267,15 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 samples (each stratum [j/M, (j+1)/M) used once, random order; DESIGN.md
  *                 reading R17; the paper's "improving the Monte Carlo integration",
  *                 PAPER.md:313). Same estimator Eq. (14); X still B(N, 1/2)-distributed.
- *   "rec_batch"   engine 1: samples per batch (0 = auto from free device memory; each sample
- *                 in flight holds 5 (d+1) fp32 planes of H x W scratch; at most 256 and 40 % of
- *                 the free device memory)
+ *   "rec_impl"    engine 1: 1 (default) tiled -- 32 x 32 tiles, the exact states entering
+ *                 each tile from per-tile summaries and a scan along every line, the blurred
+ *                 planes stay in shared memory; 0 staged -- a row pass and a
+ *                 column pass through HBM scratch. Same arithmetic, results equal to fp32
+ *                 rounding (both gated against the oracle).
+ *   "rec_batch"   engine 1: samples per batch (0 = auto from free device memory; at most 256
+ *                 and 40 % of the free device memory; each sample in flight holds, staged,
+ *                 5 (d+1) fp32 planes of H x W scratch, tiled, 16 (d+1) fp32 values per 32
+ *                 pixels of each axis' lines)
  *   "spatial_kernel" separable spatial taps on the window [-r, r], r = ceil(3 sigma_s):
  *                 0 Gaussian of Eq. (1) (default), 1 box w(m) = 1, 2 hat w(m) = r + 1 - |m|
  *                 ("any arbitrary spatial filter (such as a box or hat filter)";
@@ -291,7 +297,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value
  *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
  *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
  *   "regs", "occupancy", "alias", "variant", "spatial_kernel", "engine", "rec_batch" (last batch
- *   size), "fir_supported" (r <= 64), "sampler", "colorspace", "graph", "graph_ready", and (option "profile") "fused_ns_total",
+ *   size), "rec_impl", "fir_supported" (r <= 64), "sampler", "colorspace", "graph", "graph_ready", and (option "profile") "fused_ns_total",
  *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
  *   an unknown name.
  */

@@ -117,6 +117,33 @@ struct RecArgs {
 };
 cudaError_t launch_recursive(const RecArgs &a, cudaStream_t s);
 
+// Tiled recursive engine (recursive_tiled.cu, option "rec_impl" = 1): 32 x 32
+// tiles, exact tile-boundary states of every line from per-tile summaries and a scan, so the
+// blurred planes never leave the SM. kRecT = tile edge; per axis of nt tiles the plan keeps the
+// pole powers z_j^{L_t}, z_j^{x0_t}, z_j^{n - x0_t - L_t} (fp64-computed, stored fp32 complex).
+constexpr int kRecT = 32;
+struct RecTabs {
+    const float2 *zl;     // [2][nt]
+    const float2 *pf;     // [2][nt]
+    const float2 *pb;     // [2][nt]
+};
+struct RecTArgs {
+    const float *f;       // (d, H, W) input
+    const float *t;       // (M, d) frequency table
+    float *pz;            // (g3, d+1, H, W) partial groups
+    float mu[kMaxD];
+    int d, H, W, ntx, nty;
+    int k0, ns;           // samples [k0, k0 + ns) of this batch (batch-local index s = k - k0)
+    int g1, g3;           // sample groups of the summary passes / of the accumulation pass
+    int first;
+    RecAxis row, col;
+    float2 *Eh, *Bh;      // (ns, 2(d+1), 2, ntx, H): row tiles' causal end / anticausal start states
+    float2 *Ev, *Bv;      // (ns, 2(d+1), 2, nty, W): the same for the column tiles
+    float4 *UVh, *UVv;    // (ns, 2(d+1), 2, H) / (.., W): line states (u_{-1}, v_n)
+    RecTabs th, tv;
+};
+cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s);
+
 // Error-vs-T sweep (sweep.cu): fold partial groups into running (P', Z), S = P'/Z + mu,
 // accumulate sum (ref - S)^2 into *out (double).
 struct MuArg {
@@ -158,7 +185,10 @@ struct bf_vec_plan_s {
     int spatial = 0;           // spatial taps: 0 Gaussian (Eq. (1)), 1 box, 2 hat (reading R15)
     int engine = 0;            // 0 truncated FIR (Eq. (1) window), 1 recursive Deriche (reading R16)
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
-    float *drec = nullptr;     // recursive engine scratch (y1, y2)
+    float *drec = nullptr;     // recursive engine scratch (y1, y2; tiled: summaries)
+    int rec_impl = 1;          // recursive engine: 0 staged (row / column passes via HBM), 1 tiled
+    float2 *drtab = nullptr;   // tiled recursive engine: pole-power tables of both axes
+    size_t drtab_n = 0;
     int sampler = 0;           // 0 iid binomial draws (reading R9), 1 stratified (reading R17)
     int lab = 0;               // 1: filter in CIE-Lab (sRGB in/out, reading R18)
     float *dlab = nullptr;     // Lab copy of the input

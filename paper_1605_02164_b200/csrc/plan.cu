@@ -463,8 +463,123 @@ bf_status_t ensure_rec_scratch(bf_vec_plan_t p, int nb) {
     return BF_OK;
 }
 
+// Tiled engine: per axis of length n in tiles of kRecT, the pole powers z_j^{L_t}, z_j^{x0_t} and
+// z_j^{n - x0_t - L_t} (each exp(m (-b_j + i w_j) / sigma_s) in fp64), both axes in p->drtab.
+bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
+    const int ntx = (p->W + kRecT - 1) / kRecT, nty = (p->H + kRecT - 1) / kRecT;
+    const size_t n = (size_t)6 * (ntx + nty);
+    if (p->drtab_n != n) {
+        const double bj[2] = {1.783, 1.723}, wj[2] = {0.6318, 1.997};   // rec_axis's poles
+        std::vector<float2> h(n);
+        size_t o = 0;
+        for (int ax = 0; ax < 2; ++ax) {
+            const int len = ax == 0 ? p->W : p->H, nt = ax == 0 ? ntx : nty;
+            for (int kind = 0; kind < 3; ++kind)
+                for (int j = 0; j < 2; ++j)
+                    for (int t = 0; t < nt; ++t) {
+                        const int x0 = t * kRecT, L = std::min(kRecT, len - x0);
+                        const int m = kind == 0 ? L : kind == 1 ? x0 : len - x0 - L;
+                        const Cplx z = cexp_(-bj[j] * m / p->sigma_s, wj[j] * m / p->sigma_s);
+                        h[o++] = make_float2((float)z.r, (float)z.i);
+                    }
+        }
+        cudaFree(p->drtab);
+        p->drtab = nullptr;
+        p->drtab_n = 0;
+        BF_CUDA(cudaMalloc(&p->drtab, sizeof(float2) * n));
+        BF_CUDA(cudaMemcpy(p->drtab, h.data(), sizeof(float2) * n, cudaMemcpyHostToDevice));
+        p->drtab_n = n;
+    }
+    th->zl = p->drtab;
+    th->pf = th->zl + 2 * ntx;
+    th->pb = th->pf + 2 * ntx;
+    tv->zl = th->pb + 2 * ntx;
+    tv->pf = tv->zl + 2 * nty;
+    tv->pb = tv->pf + 2 * nty;
+    return BF_OK;
+}
+
+bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1, cudaStream_t s, int *groups_out) {
+    const int ns = k1 - k0;
+    const int NQ = 2 * (p->d + 1);
+    const int ntx = (p->W + kRecT - 1) / kRecT, nty = (p->H + kRecT - 1) / kRecT;
+    const long long tiles = (long long)ntx * nty;
+    const size_t px = (size_t)p->H * p->W;
+    // per sample in flight: row / column summaries (E, B) and line states
+    const size_t sum_h = (size_t)NQ * 2 * ntx * p->H, sum_v = (size_t)NQ * 2 * nty * p->W;
+    const size_t uv_h = (size_t)NQ * 2 * p->H, uv_v = (size_t)NQ * 2 * p->W;
+    const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v);
+    const size_t free_b = free_memory(p);
+    int nb = (int)std::max(1.0, std::min<double>(256.0, 0.4 * (double)free_b / (double)per));
+    if (p->force_batch > 0) nb = p->force_batch;
+    nb = std::min(nb, ns);
+    // sample groups: enough CTAs for ~8 per SM where the tile count alone does not give them
+    const long long want = 8LL * sm_count();
+    const int g = (int)std::min<long long>(nb, std::max<long long>(1, (want + tiles - 1) / tiles));
+    if (p->drec_bytes < per * nb) {
+        cudaFree(p->drec);
+        p->drec = nullptr;
+        p->drec_bytes = 0;
+        BF_CUDA(cudaMalloc(&p->drec, per * nb));
+        p->drec_bytes = per * nb;
+    }
+    bf_status_t st = ensure_pz(p, sizeof(float) * (size_t)g * (p->d + 1) * px);
+    if (st != BF_OK) return st;
+    RecTArgs a;
+    std::memset(&a, 0, sizeof(a));
+    st = ensure_rec_tabs(p, &a.th, &a.tv);
+    if (st != BF_OK) return st;
+    fill_mu(p);
+    a.f = f;
+    a.t = p->dt;
+    a.pz = p->dpz;
+    for (int c = 0; c < kMaxD; ++c) a.mu[c] = p->mu[c];
+    a.d = p->d;
+    a.H = p->H;
+    a.W = p->W;
+    a.ntx = ntx;
+    a.nty = nty;
+    a.g1 = g;
+    a.g3 = g;
+    float2 *base = reinterpret_cast<float2 *>(p->drec);
+    a.Eh = base;
+    a.Bh = a.Eh + (size_t)nb * sum_h;
+    a.Ev = a.Bh + (size_t)nb * sum_h;
+    a.Bv = a.Ev + (size_t)nb * sum_v;
+    a.UVh = reinterpret_cast<float4 *>(a.Bv + (size_t)nb * sum_v);
+    a.UVv = a.UVh + (size_t)nb * uv_h;
+    rec_axis(p->sigma_s, p->W, &a.row);
+    rec_axis(p->sigma_s, p->H, &a.col);
+    int slot = -1;
+    if (p->profile) {
+        if (p->ev_count == bf_vec_plan_s::kEvRing) collect_profile(p);
+        slot = p->ev_head;
+        for (int j = 0; j < 2; ++j)
+            if (!p->ev[slot][j]) BF_CUDA(cudaEventCreate(&p->ev[slot][j]));
+        BF_CUDA(cudaEventRecord(p->ev[slot][0], s));
+    }
+    for (int kb = k0; kb < k1; kb += nb) {
+        a.k0 = kb;
+        a.ns = std::min(nb, k1 - kb);
+        a.first = (kb == k0) ? 1 : 0;
+        BF_CUDA(launch_recursive_tiled(a, s));
+    }
+    if (slot >= 0) {
+        BF_CUDA(cudaEventRecord(p->ev[slot][1], s));
+        p->ev_head = (p->ev_head + 1) % bf_vec_plan_s::kEvRing;
+        p->ev_count += 1;
+    }
+    p->last_batch = nb;
+    p->last_groups = g;
+    p->last_tile_rows = kRecT;
+    p->last_ctas = tiles * g;
+    *groups_out = g;
+    return BF_OK;
+}
+
 // samples [k0, k1) of the recursive engine into p->dpz (groups = samples per batch)
 bf_status_t run_recursive(bf_vec_plan_t p, const float *f, int k0, int k1, cudaStream_t s, int *groups_out) {
+    if (p->rec_impl == 1) return run_recursive_tiled(p, f, k0, k1, s, groups_out);
     const int ns = k1 - k0;
     const size_t px = (size_t)p->H * p->W;
     // per sample in flight: y1 + y2 (2 x 2(d+1) planes) + one partial group ((d+1) planes)
@@ -586,7 +701,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         if (p->last) cudaStreamSynchronize(p->last);
         cudaFree(p->dX); cudaFree(p->dt); cudaFree(p->dQ); cudaFree(p->dgamma);
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
-        cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drun); cudaFree(p->dmse);
+        cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drtab); cudaFree(p->drun); cudaFree(p->dmse);
         cudaFree(p->dkeys); cudaFree(p->dlab); cudaFree(p->dt_batch); cudaFree(p->dX_batch);
         if (p->gexec) cudaGraphExecDestroy(p->gexec);
         for (auto &pair : p->ev)
@@ -1082,6 +1197,11 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         p->sampler = (int)v;   // takes effect at the next bf_vec_sample_freqs
         return BF_OK;
     }
+    if (!std::strcmp(name, "rec_impl")) {
+        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        p->rec_impl = (int)v;
+        return BF_OK;
+    }
     if (!std::strcmp(name, "rec_batch")) { if (v < 0) return BF_E_ARG; p->force_batch = (int)v; return BF_OK; }
     if (!std::strcmp(name, "spatial_kernel")) {
         if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
@@ -1114,7 +1234,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"sampler", p->sampler}, {"colorspace", p->lab},
+        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"sampler", p->sampler}, {"colorspace", p->lab},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)

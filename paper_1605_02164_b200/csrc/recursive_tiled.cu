@@ -1,0 +1,355 @@
+// recursive_tiled.cu -- the O(1)-in-sigma_s engine without intermediate images in HBM
+// (option "rec_impl" = 1, the default of engine 1).
+//
+// Same arithmetic as recursive.cu ("using separability and recursion ... at O(1)
+// cost with respect to sigma_s"; Deriche kernel, reading R16; reflected-periodic lines, R1):
+// per line x[0..n-1] and pole z_j,
+//   u_j[k] = x[k] + z_j u_j[k-1],  v_j[k] = x[k] + z_j v_j[k+1],  y[k] = sum_j Re[A_j (u_j + v_j)] - g0 x[k],
+//   u_j[-1] = (S_head + z^n S_tail) / (1 - z^2n),  v_j[n] = u_j[n-1].
+// The image is cut into 32 x 32 tiles. By linearity a tile's segment of a line only needs the two
+// states entering it, u[x0-1] and v[x0+L], and those follow from per-tile summaries
+//   e_t = sum_m z^{L-1-m} x[x0+m]  (causal end state from zero),  b_t = sum_m z^m x[x0+m]
+// by a scan along the line:  u[x0_{t+1}-1] = z^{L_t} u[x0_t-1] + e_t,  v[x0_{t-1}+L] = z^{L_t} v[x0_t+L] + b_t,
+// with S_tail / S_head the zero-started scans' final values (exact: no head / tail truncation).
+// Per batch of samples:
+//   pass 0 (tile)  : modulate (Alg. 1), row summaries e, b of the 2(d+1) planes
+//   scan rows      : zero-started row states per tile + (u_{-1}, v_n) per row
+//   pass 1 (tile)  : exact row blur of the tile into shared memory, column summaries
+//   scan columns   : the same along columns
+//   pass 2 (tile)  : exact row blur, exact column blur, Re[conj(H) blur] (Alg. 1) summed
+//                    over the group's samples in registers, one partial plane set per group.
+// HBM sees f, the summaries (8 B per pixel-sample per axis) and the partial sums only.
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "kernel_common.cuh"
+
+namespace bfvec {
+namespace {
+
+constexpr int T = kRecT;
+constexpr int TP = T + 1;
+
+struct St {              // both poles, (c-part, s-part) of one pair of planes
+    float2 ur[2], ui[2];
+};
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 fma2s(float w, float2 v, float2 acc) {
+    return __ffma2_rn(make_float2(w, w), v, acc);
+}
+__device__ __forceinline__ float2 mul2s(float w, float2 v) { return __fmul2_rn(make_float2(w, w), v); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return f2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return f2(a.x + b.x, a.y + b.y); }
+
+__device__ __forceinline__ void zero(St &s) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) s.ur[j] = s.ui[j] = f2(0.f, 0.f);
+}
+// u <- x + z u for both poles
+__device__ __forceinline__ void step(const RecAxis &ax, St &s, float2 x) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const float2 ur = s.ur[j], ui = s.ui[j];
+        s.ur[j] = fma2s(ax.zr[j], ur, fma2s(-ax.zi[j], ui, x));
+        s.ui[j] = fma2s(ax.zr[j], ui, mul2s(ax.zi[j], ur));
+    }
+}
+// sum_j Re[A_j u_j]
+__device__ __forceinline__ float2 re_a(const RecAxis &ax, const St &s) {
+    float2 y = mul2s(ax.ar[0], s.ur[0]);
+    y = fma2s(-ax.ai[0], s.ui[0], y);
+    y = fma2s(ax.ar[1], s.ur[1], y);
+    y = fma2s(-ax.ai[1], s.ui[1], y);
+    return y;
+}
+
+// summary / state arrays: (s, q, j, tile, line) and (s, q, j, line)
+__device__ __forceinline__ long long sidx(int s, int q, int j, int t, int line, int NQ, int nt, int nlines) {
+    return ((((long long)s * NQ + q) * 2 + j) * nt + t) * nlines + line;
+}
+__device__ __forceinline__ long long uidx(int s, int q, int j, int line, int NQ, int nlines) {
+    return (((long long)s * NQ + q) * 2 + j) * nlines + line;
+}
+
+// store the pair's two planes' state (q = 2p: .x parts, q = 2p + 1: .y parts) for both poles
+__device__ __forceinline__ void put_state(float2 *A, const St &s, int b, int p, int t, int line, int NQ, int nt,
+                                          int nlines) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        A[sidx(b, 2 * p, j, t, line, NQ, nt, nlines)] = f2(s.ur[j].x, s.ui[j].x);
+        A[sidx(b, 2 * p + 1, j, t, line, NQ, nt, nlines)] = f2(s.ur[j].y, s.ui[j].y);
+    }
+}
+// the exact states entering tile t of a line from the scanned zero-started ones:
+// L = Lz + z^{x0} u_{-1},  R = Rz + z^{n - x0 - L} v_n
+__device__ __forceinline__ void get_states(const float2 *E, const float2 *B, const float4 *UV, const RecTabs &tb,
+                                           int b, int p, int t, int line, int NQ, int nt, int nlines, St &L,
+                                           St &R) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const float2 pf = tb.pf[j * nt + t], pb = tb.pb[j * nt + t];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = 2 * p + h;
+            const float2 e = E[sidx(b, q, j, t, line, NQ, nt, nlines)];
+            const float2 bb = B[sidx(b, q, j, t, line, NQ, nt, nlines)];
+            const float4 uv = UV[uidx(b, q, j, line, NQ, nlines)];
+            const float2 l = cadd(e, cmul(pf, f2(uv.x, uv.y)));
+            const float2 r = cadd(bb, cmul(pb, f2(uv.z, uv.w)));
+            if (h == 0) {
+                L.ur[j].x = l.x; L.ui[j].x = l.y; R.ur[j].x = r.x; R.ui[j].x = r.y;
+            } else {
+                L.ur[j].y = l.x; L.ui[j].y = l.y; R.ur[j].y = r.x; R.ui[j].y = r.y;
+            }
+        }
+    }
+}
+
+template <int NP, int MODE>
+struct TileSmem {
+    static constexpr int D = NP - 1, NQ = 2 * NP;
+    static constexpr int OFF_CS = D * T * TP;                 // floats; fs[D][T][TP] first
+    static constexpr int OFF_RB = OFF_CS + 2 * T * TP;        // cs: [T][TP] float2
+    static constexpr size_t BYTES = sizeof(float) * (size_t)(OFF_RB + (MODE >= 1 ? NQ * T * TP : 0));
+};
+
+// One 32 x 32 tile x one group of samples. Warp p owns the pair p of planes: (c, s) for p = 0
+// (-> Z), (c f_{p-1}, s f_{p-1}) otherwise (-> P_{p-1}); lane = row in the row stage, column in
+// the column stage.
+template <int NP, int MODE>
+__global__ void __launch_bounds__(32 * NP) rect_tile_kernel(const __grid_constant__ RecTArgs a) {
+    using L = TileSmem<NP, MODE>;
+    constexpr int D = L::D, NQ = L::NQ;
+    extern __shared__ float sm[];
+    float *fs = sm;
+    float2 *cs = reinterpret_cast<float2 *>(sm + L::OFF_CS);
+    float *rb = sm + L::OFF_RB;
+
+    const int tid = threadIdx.x, lane = tid & 31, p = tid >> 5;
+    const int tx = blockIdx.x % a.ntx, ty = blockIdx.x / a.ntx;
+    const int x0 = tx * T, y0 = ty * T;
+    const int H = a.H, W = a.W;
+    const int Lx = min(T, W - x0), Ly = min(T, H - y0);
+    const long long plane = (long long)H * W;
+    const int G = (MODE == 2) ? a.g3 : a.g1, g = blockIdx.y;
+    const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
+
+    for (int e = tid; e < D * T * T; e += 32 * NP) {   // centred f tile (reading R12), zeros outside
+        const int c = e / (T * T), i = (e / T) % T, j = e % T;
+        fs[(c * T + i) * TP + j] =
+            (i < Ly && j < Lx) ? a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c] : 0.f;
+    }
+    float acc[T];
+#pragma unroll
+    for (int m = 0; m < T; ++m) acc[m] = 0.f;
+
+    // the pair's real input at (row i, column j) of the tile
+    auto xin = [&](int i, int j) -> float2 {
+        const float2 h = cs[i * TP + j];
+        if (p == 0) return h;
+        const float fv = fs[((p - 1) * T + i) * TP + j];
+        return f2(h.x * fv, h.y * fv);
+    };
+
+    for (int b = s0; b < s1; ++b) {
+        const int k = a.k0 + b;
+        float tk[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) tk[c] = a.t[(long long)k * D + c];
+        St rl, rr;
+        if (MODE >= 1 && lane < Ly)   // issued before the modulation; used by the row stage
+            get_states(a.Eh, a.Bh, a.UVh, a.th, b, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
+        __syncthreads();   // the previous sample's stages are done with cs / rb (and fs is complete)
+        for (int e = tid; e < T * T; e += 32 * NP) {
+            const int i = e / T, j = e % T;
+            float th = 0.f;
+#pragma unroll
+            for (int c = 0; c < D; ++c) th = fmaf(tk[c], fs[(c * T + i) * TP + j], th);
+            float sn, cn;
+            __sincosf(th, &sn, &cn);
+            cs[i * TP + j] = f2(cn, sn);
+        }
+        __syncthreads();
+
+        // ---- row stage: lane = row ----
+        if (lane < Ly) {
+            const RecAxis &ax = a.row;
+            const int y = y0 + lane;
+            if (MODE == 0) {
+                St st;
+                zero(st);
+                for (int m = 0; m < Lx; ++m) step(ax, st, xin(lane, m));
+                put_state(a.Eh, st, b, p, tx, y, NQ, a.ntx, H);
+                zero(st);
+                for (int m = Lx - 1; m >= 0; --m) step(ax, st, xin(lane, m));
+                put_state(a.Bh, st, b, p, tx, y, NQ, a.ntx, H);
+            } else {
+                float *r0 = rb + (2 * p * T + lane) * TP, *r1 = rb + ((2 * p + 1) * T + lane) * TP;
+                St st = rl;
+                for (int m = 0; m < Lx; ++m) {
+                    const float2 x = xin(lane, m);
+                    step(ax, st, x);
+                    const float2 yv = fma2s(-ax.g0, x, re_a(ax, st));
+                    r0[m] = yv.x;
+                    r1[m] = yv.y;
+                }
+                st = rr;
+                for (int m = Lx - 1; m >= 0; --m) {
+                    step(ax, st, xin(lane, m));
+                    const float2 r = re_a(ax, st);
+                    r0[m] += r.x;
+                    r1[m] += r.y;
+                }
+            }
+        }
+        if (MODE == 0) continue;
+        __syncthreads();
+
+        // ---- column stage: lane = column ----
+        if (lane < Lx) {
+            const RecAxis &ax = a.col;
+            const int x = x0 + lane;
+            const float *c0 = rb + 2 * p * T * TP + lane, *c1 = rb + (2 * p + 1) * T * TP + lane;
+            if (MODE == 1) {
+                St st;
+                zero(st);
+                for (int m = 0; m < Ly; ++m) step(ax, st, f2(c0[m * TP], c1[m * TP]));
+                put_state(a.Ev, st, b, p, ty, x, NQ, a.nty, W);
+                zero(st);
+                for (int m = Ly - 1; m >= 0; --m) step(ax, st, f2(c0[m * TP], c1[m * TP]));
+                put_state(a.Bv, st, b, p, ty, x, NQ, a.nty, W);
+            } else {
+                St cl, cr;
+                get_states(a.Ev, a.Bv, a.UVv, a.tv, b, p, ty, x, NQ, a.nty, W, cl, cr);
+                St st = cl;
+#pragma unroll
+                for (int m = 0; m < T; ++m) {
+                    if (m < Ly) {
+                        const float2 xv = f2(c0[m * TP], c1[m * TP]);
+                        step(ax, st, xv);
+                        const float2 yv = fma2s(-ax.g0, xv, re_a(ax, st));
+                        const float2 h = cs[m * TP + lane];
+                        acc[m] = fmaf(h.x, yv.x, fmaf(h.y, yv.y, acc[m]));   // Re[conj(H) blur]
+                    }
+                }
+                st = cr;
+#pragma unroll
+                for (int m = T - 1; m >= 0; --m) {
+                    if (m < Ly) {
+                        step(ax, st, f2(c0[m * TP], c1[m * TP]));
+                        const float2 r = re_a(ax, st);
+                        const float2 h = cs[m * TP + lane];
+                        acc[m] = fmaf(h.x, r.x, fmaf(h.y, r.y, acc[m]));
+                    }
+                }
+            }
+        }
+    }
+    if (MODE == 2 && lane < Lx) {
+        const int pl = (p == 0) ? D : p - 1;
+        float *dst = a.pz + ((long long)g * (D + 1) + pl) * plane + (long long)y0 * W + x0 + lane;
+#pragma unroll
+        for (int m = 0; m < T; ++m)
+            if (m < Ly) dst[(long long)m * W] = a.first ? acc[m] : dst[(long long)m * W] + acc[m];
+    }
+}
+
+// One thread per (sample, plane, pole, line): zero-started scans over the line's tiles in both
+// directions (replacing the summaries in place by the states entering each tile), then the
+// line's exact reflected-periodic states (u_{-1}, v_n).
+// Loads are issued kScanB tiles at a time (independent of the running state) so each thread keeps
+// kScanB requests in flight instead of one dependent load per tile.
+constexpr int kScanB = 8;
+__global__ void __launch_bounds__(256) rect_scan_kernel(float2 *__restrict__ E, float2 *__restrict__ B,
+                                                        float4 *__restrict__ UV, const RecTabs tb,
+                                                        const RecAxis ax, int nt, int nlines, long long nthreads) {
+    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= nthreads) return;
+    const int line = (int)(id % nlines);
+    const long long sqj = id / nlines;   // (s * NQ + q) * 2 + j
+    const int j = (int)(sqj & 1);
+    const long long base = sqj * nt * nlines + line;
+    const float2 *zl = tb.zl + j * nt;
+    float2 c = f2(0.f, 0.f);
+    for (int t0 = 0; t0 < nt; t0 += kScanB) {
+        float2 v[kScanB];
+#pragma unroll
+        for (int u = 0; u < kScanB; ++u)
+            if (t0 + u < nt) v[u] = E[base + (long long)(t0 + u) * nlines];
+#pragma unroll
+        for (int u = 0; u < kScanB; ++u)
+            if (t0 + u < nt) {
+                E[base + (long long)(t0 + u) * nlines] = c;
+                c = cadd(cmul(zl[t0 + u], c), v[u]);
+            }
+    }
+    const float2 s_tail = c;
+    c = f2(0.f, 0.f);
+    for (int t1 = nt - 1; t1 >= 0; t1 -= kScanB) {
+        float2 v[kScanB];
+#pragma unroll
+        for (int u = 0; u < kScanB; ++u)
+            if (t1 - u >= 0) v[u] = B[base + (long long)(t1 - u) * nlines];
+#pragma unroll
+        for (int u = 0; u < kScanB; ++u)
+            if (t1 - u >= 0) {
+                B[base + (long long)(t1 - u) * nlines] = c;
+                c = cadd(cmul(zl[t1 - u], c), v[u]);
+            }
+    }
+    const float2 s_head = c;
+    const float2 zn = j ? f2(ax.znr[1], ax.zni[1]) : f2(ax.znr[0], ax.zni[0]);   // no dynamic param indexing
+    const float2 inv = j ? f2(ax.invr[1], ax.invi[1]) : f2(ax.invr[0], ax.invi[0]);
+    const float2 um1 = cmul(cadd(s_head, cmul(zn, s_tail)), inv);
+    const float2 vn = cadd(s_tail, cmul(zn, um1));
+    UV[sqj * nlines + line] = make_float4(um1.x, um1.y, vn.x, vn.y);
+}
+
+template <int NP, int MODE>
+cudaError_t launch_tile(const RecTArgs &a, int groups, cudaStream_t s) {
+    const size_t smem = TileSmem<NP, MODE>::BYTES;
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = ensure_smem_attr(rect_tile_kernel<NP, MODE>, smem, attr);
+    if (e != cudaSuccess) return e;
+    rect_tile_kernel<NP, MODE><<<dim3(a.ntx * a.nty, groups), 32 * NP, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan(float2 *E, float2 *B, float4 *UV, const RecTabs &tb, const RecAxis &ax, int nt, int nlines,
+                        long long nq, cudaStream_t s) {
+    const long long n = nq * 2 * nlines;
+    rect_scan_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(E, B, UV, tb, ax, nt, nlines, n);
+    return cudaGetLastError();
+}
+
+template <int NP>
+cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
+    const long long nq = (long long)a.ns * 2 * NP;
+    cudaError_t e = launch_tile<NP, 0>(a, a.g1, s);
+    if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.H, nq, s);
+    if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
+    if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
+    if (e == cudaSuccess) e = launch_tile<NP, 2>(a, a.g3, s);
+    return e;
+}
+
+}  // namespace
+
+cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s) {
+    switch (a.d) {
+        case 1: return launch_np<2>(a, s);
+        case 2: return launch_np<3>(a, s);
+        case 3: return launch_np<4>(a, s);
+        case 4: return launch_np<5>(a, s);
+        case 5: return launch_np<6>(a, s);
+        case 6: return launch_np<7>(a, s);
+        case 7: return launch_np<8>(a, s);
+        case 8: return launch_np<9>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace bfvec

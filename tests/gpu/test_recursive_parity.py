@@ -17,9 +17,20 @@ from workloads.configs import random_image, small_config
 pytestmark = pytest.mark.gpu
 
 
+_IMPL = {"rec_impl": 1}
+
+
+@pytest.fixture(autouse=True, params=[1, 0], ids=["tiled", "staged"])
+def rec_impl(request):
+    """Every test runs on both implementations of the engine (option "rec_impl")."""
+    _IMPL["rec_impl"] = request.param
+    yield request.param
+
+
 def _rec_plan(cfg, batch=0):
     p = H.gpu_plan(cfg)
     p.set_option("engine", 1)
+    p.set_option("rec_impl", _IMPL["rec_impl"])
     if batch:
         p.set_option("rec_batch", batch)
     return p
@@ -34,7 +45,7 @@ def test_config_full_parity(i):
     p = _rec_plan(cfg)
     S_g, P_g, Z_g = H.gpu_run(p, f)
     res = H.gates(cfg, S_g, P_g, Z_g, S_o, P_o, Z_o)
-    print(f"recursive config {i}: {res} batch {p.info('rec_batch')}")
+    print(f"recursive config {i} impl {p.info('rec_impl')}: {res} batch {p.info('rec_batch')}")
     H.assert_gates(res)
 
 
