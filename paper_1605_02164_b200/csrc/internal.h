@@ -126,6 +126,7 @@ struct RecTabs {
     const float2 *zl;     // [2][nt]
     const float2 *pf;     // [2][nt]
     const float2 *pb;     // [2][nt]
+    const float4 *zp;     // [kRecT]: (z_0^m, z_1^m), m = 0 .. kRecT-1
 };
 struct RecTArgs {
     const float *f;       // (d, H, W) input

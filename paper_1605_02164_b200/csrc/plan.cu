@@ -467,7 +467,7 @@ bf_status_t ensure_rec_scratch(bf_vec_plan_t p, int nb) {
 // z_j^{n - x0_t - L_t} (each exp(m (-b_j + i w_j) / sigma_s) in fp64), both axes in p->drtab.
 bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
     const int ntx = (p->W + kRecT - 1) / kRecT, nty = (p->H + kRecT - 1) / kRecT;
-    const size_t n = (size_t)6 * (ntx + nty);
+    const size_t n = (size_t)6 * (ntx + nty) + 2 * kRecT;   // + zp: (z_0^m, z_1^m), m < kRecT
     if (p->drtab_n != n) {
         const double bj[2] = {1.783, 1.723}, wj[2] = {0.6318, 1.997};   // rec_axis's poles
         std::vector<float2> h(n);
@@ -483,6 +483,11 @@ bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
                         h[o++] = make_float2((float)z.r, (float)z.i);
                     }
         }
+        for (int m = 0; m < kRecT; ++m)
+            for (int j = 0; j < 2; ++j) {
+                const Cplx z = cexp_(-bj[j] * m / p->sigma_s, wj[j] * m / p->sigma_s);
+                h[o++] = make_float2((float)z.r, (float)z.i);
+            }
         cudaFree(p->drtab);
         p->drtab = nullptr;
         p->drtab_n = 0;
@@ -496,6 +501,7 @@ bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
     tv->zl = th->pb + 2 * ntx;
     tv->pf = tv->zl + 2 * nty;
     tv->pb = tv->pf + 2 * nty;
+    th->zp = tv->zp = reinterpret_cast<const float4 *>(tv->pb + 2 * nty);
     return BF_OK;
 }
 

@@ -113,14 +113,93 @@ struct TileSmem {
     static constexpr int D = NP - 1, NQ = 2 * NP;
     static constexpr int OFF_CS = D * T * TP;                 // floats; fs[D][T][TP] first
     static constexpr int OFF_RB = OFF_CS + 2 * T * TP;        // cs: [T][TP] float2
-    static constexpr size_t BYTES = sizeof(float) * (size_t)(OFF_RB + (MODE >= 1 ? NQ * T * TP : 0));
+    static constexpr int OFF_ZP = OFF_RB + (MODE >= 1 ? NQ * T * TP : 0);   // zp[2 axes][T] float4
+    static constexpr int OFF_ACC = OFF_ZP + 2 * 4 * T;                     // MODE 2: acc[NP][T][T]
+    static constexpr size_t BYTES = sizeof(float) * (size_t)(OFF_ACC + (MODE == 2 ? NP * T * T : 0));
 };
 
-// One 32 x 32 tile x one group of samples. Warp p owns the pair p of planes: (c, s) for p = 0
-// (-> Z), (c f_{p-1}, s f_{p-1}) otherwise (-> P_{p-1}); lane = row in the row stage, column in
-// the column stage.
+// zero-started summaries of one pair over a segment of n <= T elements,
+//   e = sum_m z^{n-1-m} x[m]  (the causal state after the segment),  b = sum_m z^m x[m],
+// as dot products with zp[m] = (z_0^m, z_1^m) -- no dependency chain along the segment.
+template <bool FULL, class X>
+__device__ __forceinline__ void summaries(const float4 *zp, int n, X xat, St &e, St &b) {
+    zero(e);
+    zero(b);
+#pragma unroll 8
+    for (int m = 0; m < T; ++m) {
+        if (FULL || m < n) {
+            const float2 x = xat(m);
+            const float4 pb = zp[m], pe = zp[(FULL ? T : n) - 1 - m];
+            b.ur[0] = fma2s(pb.x, x, b.ur[0]);
+            b.ui[0] = fma2s(pb.y, x, b.ui[0]);
+            b.ur[1] = fma2s(pb.z, x, b.ur[1]);
+            b.ui[1] = fma2s(pb.w, x, b.ui[1]);
+            e.ur[0] = fma2s(pe.x, x, e.ur[0]);
+            e.ui[0] = fma2s(pe.y, x, e.ui[0]);
+            e.ur[1] = fma2s(pe.z, x, e.ur[1]);
+            e.ui[1] = fma2s(pe.w, x, e.ui[1]);
+        }
+    }
+}
+
+// exact blur of one pair along a segment from its entering states: r0/r1[m * stride] (the two
+// planes) <- sum_j Re[A_j (u_j + v_j)] - g0 x
+template <bool FULL, class X>
+__device__ __forceinline__ void blur_segment(const RecAxis &ax, int n, X xat, const St &l, const St &r, float *r0,
+                                             float *r1) {
+    St st = l;
+#pragma unroll 8
+    for (int m = 0; m < T; ++m) {
+        if (FULL || m < n) {
+            const float2 x = xat(m);
+            step(ax, st, x);
+            const float2 yv = fma2s(-ax.g0, x, re_a(ax, st));
+            r0[m] = yv.x;
+            r1[m] = yv.y;
+        }
+    }
+    st = r;
+#pragma unroll 8
+    for (int m = T - 1; m >= 0; --m) {
+        if (FULL || m < n) {
+            step(ax, st, xat(m));
+            const float2 v = re_a(ax, st);
+            r0[m] += v.x;
+            r1[m] += v.y;
+        }
+    }
+}
+
+// exact column blur of one pair, folded into acc[m * 32] += Re[conj(H) blur] (Alg. 1);
+// acc is this thread's column of the group's shared-memory accumulator
+template <bool FULL>
+__device__ __forceinline__ void blur_accumulate(const RecAxis &ax, int n, const float *c0, const float *c1,
+                                                const float2 *h, const St &l, const St &r, float *acc) {
+    St st = l;
+#pragma unroll 8
+    for (int m = 0; m < T; ++m) {
+        if (FULL || m < n) {
+            const float2 xv = f2(c0[m * TP], c1[m * TP]);
+            step(ax, st, xv);
+            const float2 yv = fma2s(-ax.g0, xv, re_a(ax, st));
+            const float2 hm = h[m * TP];
+            acc[m * T] = fmaf(hm.x, yv.x, fmaf(hm.y, yv.y, acc[m * T]));
+        }
+    }
+    st = r;
+#pragma unroll 8
+    for (int m = T - 1; m >= 0; --m) {
+        if (FULL || m < n) {
+            step(ax, st, f2(c0[m * TP], c1[m * TP]));
+            const float2 v = re_a(ax, st);
+            const float2 hm = h[m * TP];
+            acc[m * T] = fmaf(hm.x, v.x, fmaf(hm.y, v.y, acc[m * T]));
+        }
+    }
+}
+
 template <int NP, int MODE>
-__global__ void __launch_bounds__(32 * NP) rect_tile_kernel(const __grid_constant__ RecTArgs a) {
+__global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(const __grid_constant__ RecTArgs a) {
     using L = TileSmem<NP, MODE>;
     constexpr int D = L::D, NQ = L::NQ;
     extern __shared__ float sm[];
@@ -137,14 +216,16 @@ __global__ void __launch_bounds__(32 * NP) rect_tile_kernel(const __grid_constan
     const int G = (MODE == 2) ? a.g3 : a.g1, g = blockIdx.y;
     const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
 
+    float4 *zp = reinterpret_cast<float4 *>(sm + L::OFF_ZP);   // [0][m]: row axis, [1][m]: column axis
+    if (tid < 2 * T) zp[tid] = (tid < T) ? a.th.zp[tid] : a.tv.zp[tid - T];
     for (int e = tid; e < D * T * T; e += 32 * NP) {   // centred f tile (reading R12), zeros outside
         const int c = e / (T * T), i = (e / T) % T, j = e % T;
         fs[(c * T + i) * TP + j] =
             (i < Ly && j < Lx) ? a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c] : 0.f;
     }
-    float acc[T];
-#pragma unroll
-    for (int m = 0; m < T; ++m) acc[m] = 0.f;
+    float *acc = sm + L::OFF_ACC + p * T * T + lane;   // MODE 2: this thread's column of pair p
+    if (MODE == 2)
+        for (int m = 0; m < T; ++m) acc[m * T] = 0.f;
 
     // the pair's real input at (row i, column j) of the tile
     auto xin = [&](int i, int j) -> float2 {
@@ -175,34 +256,27 @@ __global__ void __launch_bounds__(32 * NP) rect_tile_kernel(const __grid_constan
         __syncthreads();
 
         // ---- row stage: lane = row ----
+        const bool full = Lx == T && Ly == T;
         if (lane < Ly) {
-            const RecAxis &ax = a.row;
+            const float2 *hrow = cs + lane * TP;
+            const float *frow = fs + ((p > 0 ? p - 1 : 0) * T + lane) * TP;
+            auto xat = [&](int m) -> float2 {   // the pair's real input at column m of this row
+                const float2 h = hrow[m];
+                if (p == 0) return h;
+                const float fv = frow[m];
+                return f2(h.x * fv, h.y * fv);
+            };
             const int y = y0 + lane;
             if (MODE == 0) {
-                St st;
-                zero(st);
-                for (int m = 0; m < Lx; ++m) step(ax, st, xin(lane, m));
-                put_state(a.Eh, st, b, p, tx, y, NQ, a.ntx, H);
-                zero(st);
-                for (int m = Lx - 1; m >= 0; --m) step(ax, st, xin(lane, m));
-                put_state(a.Bh, st, b, p, tx, y, NQ, a.ntx, H);
+                St e, bb;
+                if (full) summaries<true>(zp, T, xat, e, bb);
+                else summaries<false>(zp, Lx, xat, e, bb);
+                put_state(a.Eh, e, b, p, tx, y, NQ, a.ntx, H);
+                put_state(a.Bh, bb, b, p, tx, y, NQ, a.ntx, H);
             } else {
                 float *r0 = rb + (2 * p * T + lane) * TP, *r1 = rb + ((2 * p + 1) * T + lane) * TP;
-                St st = rl;
-                for (int m = 0; m < Lx; ++m) {
-                    const float2 x = xin(lane, m);
-                    step(ax, st, x);
-                    const float2 yv = fma2s(-ax.g0, x, re_a(ax, st));
-                    r0[m] = yv.x;
-                    r1[m] = yv.y;
-                }
-                st = rr;
-                for (int m = Lx - 1; m >= 0; --m) {
-                    step(ax, st, xin(lane, m));
-                    const float2 r = re_a(ax, st);
-                    r0[m] += r.x;
-                    r1[m] += r.y;
-                }
+                if (full) blur_segment<true>(a.row, T, xat, rl, rr, r0, r1);
+                else blur_segment<false>(a.row, Lx, xat, rl, rr, r0, r1);
             }
         }
         if (MODE == 0) continue;
@@ -210,50 +284,27 @@ __global__ void __launch_bounds__(32 * NP) rect_tile_kernel(const __grid_constan
 
         // ---- column stage: lane = column ----
         if (lane < Lx) {
-            const RecAxis &ax = a.col;
             const int x = x0 + lane;
             const float *c0 = rb + 2 * p * T * TP + lane, *c1 = rb + (2 * p + 1) * T * TP + lane;
             if (MODE == 1) {
-                St st;
-                zero(st);
-                for (int m = 0; m < Ly; ++m) step(ax, st, f2(c0[m * TP], c1[m * TP]));
-                put_state(a.Ev, st, b, p, ty, x, NQ, a.nty, W);
-                zero(st);
-                for (int m = Ly - 1; m >= 0; --m) step(ax, st, f2(c0[m * TP], c1[m * TP]));
-                put_state(a.Bv, st, b, p, ty, x, NQ, a.nty, W);
+                auto xat = [&](int m) -> float2 { return f2(c0[m * TP], c1[m * TP]); };
+                St e, bb;
+                if (full) summaries<true>(zp + T, T, xat, e, bb);
+                else summaries<false>(zp + T, Ly, xat, e, bb);
+                put_state(a.Ev, e, b, p, ty, x, NQ, a.nty, W);
+                put_state(a.Bv, bb, b, p, ty, x, NQ, a.nty, W);
             } else {
                 St cl, cr;
                 get_states(a.Ev, a.Bv, a.UVv, a.tv, b, p, ty, x, NQ, a.nty, W, cl, cr);
-                St st = cl;
-#pragma unroll
-                for (int m = 0; m < T; ++m) {
-                    if (m < Ly) {
-                        const float2 xv = f2(c0[m * TP], c1[m * TP]);
-                        step(ax, st, xv);
-                        const float2 yv = fma2s(-ax.g0, xv, re_a(ax, st));
-                        const float2 h = cs[m * TP + lane];
-                        acc[m] = fmaf(h.x, yv.x, fmaf(h.y, yv.y, acc[m]));   // Re[conj(H) blur]
-                    }
-                }
-                st = cr;
-#pragma unroll
-                for (int m = T - 1; m >= 0; --m) {
-                    if (m < Ly) {
-                        step(ax, st, f2(c0[m * TP], c1[m * TP]));
-                        const float2 r = re_a(ax, st);
-                        const float2 h = cs[m * TP + lane];
-                        acc[m] = fmaf(h.x, r.x, fmaf(h.y, r.y, acc[m]));
-                    }
-                }
+                if (full) blur_accumulate<true>(a.col, T, c0, c1, cs + lane, cl, cr, acc);
+                else blur_accumulate<false>(a.col, Ly, c0, c1, cs + lane, cl, cr, acc);
             }
         }
     }
     if (MODE == 2 && lane < Lx) {
         const int pl = (p == 0) ? D : p - 1;
         float *dst = a.pz + ((long long)g * (D + 1) + pl) * plane + (long long)y0 * W + x0 + lane;
-#pragma unroll
-        for (int m = 0; m < T; ++m)
-            if (m < Ly) dst[(long long)m * W] = a.first ? acc[m] : dst[(long long)m * W] + acc[m];
+        for (int m = 0; m < Ly; ++m) dst[(long long)m * W] = a.first ? acc[m * T] : dst[(long long)m * W] + acc[m * T];
     }
 }
 
@@ -262,7 +313,7 @@ __global__ void __launch_bounds__(32 * NP) rect_tile_kernel(const __grid_constan
 // line's exact reflected-periodic states (u_{-1}, v_n).
 // Loads are issued kScanB tiles at a time (independent of the running state) so each thread keeps
 // kScanB requests in flight instead of one dependent load per tile.
-constexpr int kScanB = 8;
+constexpr int kScanB = 16;
 __global__ void __launch_bounds__(256) rect_scan_kernel(float2 *__restrict__ E, float2 *__restrict__ B,
                                                         float4 *__restrict__ UV, const RecTabs tb,
                                                         const RecAxis ax, int nt, int nlines, long long nthreads) {
