@@ -384,7 +384,8 @@ def run_ours(args, cfg):
     achieved = flops / (fused_ms / 1e3) / 1e12
     kname = KERNEL_NAMES.get(plan.info("variant"), "mcsf_fused_kernel")
     if args.engine == 1:
-        kname = "rec_row_kernel+rec_col_kernel"
+        kname = ("rect_tile_kernel x3 + rect_scan_kernel x2" if plan.info("rec_impl") == 1
+                 else "rec_row_kernel+rec_col_kernel")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": measured_traffic(cfg, kname, units_per_launch,
                                         {"tile_rows": plan.info("tile_rows"), "groups": plan.info("groups")}),

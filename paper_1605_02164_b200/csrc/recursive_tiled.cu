@@ -240,9 +240,11 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
         float tk[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) tk[c] = a.t[(long long)k * D + c];
-        St rl, rr;
+        St rl, rr, cl, cr;
         if (MODE >= 1 && lane < Ly)   // issued before the modulation; used by the row stage
             get_states(a.Eh, a.Bh, a.UVh, a.th, b, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
+        if (MODE == 2 && lane < Lx)   // the column stage's, in flight during the row stage
+            get_states(a.Ev, a.Bv, a.UVv, a.tv, b, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
         __syncthreads();   // the previous sample's stages are done with cs / rb (and fs is complete)
         for (int e = tid; e < T * T; e += 32 * NP) {
             const int i = e / T, j = e % T;
@@ -294,8 +296,6 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
                 put_state(a.Ev, e, b, p, ty, x, NQ, a.nty, W);
                 put_state(a.Bv, bb, b, p, ty, x, NQ, a.nty, W);
             } else {
-                St cl, cr;
-                get_states(a.Ev, a.Bv, a.UVv, a.tv, b, p, ty, x, NQ, a.nty, W, cl, cr);
                 if (full) blur_accumulate<true>(a.col, T, c0, c1, cs + lane, cl, cr, acc);
                 else blur_accumulate<false>(a.col, Ly, c0, c1, cs + lane, cl, cr, acc);
             }
@@ -308,50 +308,49 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
     }
 }
 
-// One thread per (sample, plane, pole, line): zero-started scans over the line's tiles in both
-// directions (replacing the summaries in place by the states entering each tile), then the
-// line's exact reflected-periodic states (u_{-1}, v_n).
+// One chain per (sample, plane, pole, line), two threads per chain: threads [0, 128) of a block run
+// the zero-started causal scan over the line's tiles, threads [128, 256) the anticausal one, for
+// the same 128 chains (each replaces the summaries in place by the states entering each tile);
+// then the line's exact reflected-periodic states (u_{-1}, v_n) from both scans' final values.
 // Loads are issued kScanB tiles at a time (independent of the running state) so each thread keeps
 // kScanB requests in flight instead of one dependent load per tile.
 constexpr int kScanB = 16;
 __global__ void __launch_bounds__(256) rect_scan_kernel(float2 *__restrict__ E, float2 *__restrict__ B,
                                                         float4 *__restrict__ UV, const RecTabs tb,
-                                                        const RecAxis ax, int nt, int nlines, long long nthreads) {
-    const long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (id >= nthreads) return;
+                                                        const RecAxis ax, int nt, int nlines, long long nchains) {
+    __shared__ float2 fin[2][128];
+    const int dir = threadIdx.x >> 7;
+    const long long id = (long long)blockIdx.x * 128 + (threadIdx.x & 127);
+    const bool live = id < nchains;
     const int line = (int)(id % nlines);
     const long long sqj = id / nlines;   // (s * NQ + q) * 2 + j
     const int j = (int)(sqj & 1);
     const long long base = sqj * nt * nlines + line;
     const float2 *zl = tb.zl + j * nt;
+    float2 *A = dir ? B : E;
     float2 c = f2(0.f, 0.f);
-    for (int t0 = 0; t0 < nt; t0 += kScanB) {
-        float2 v[kScanB];
+    if (live) {
+        for (int i0 = 0; i0 < nt; i0 += kScanB) {
+            float2 v[kScanB];
 #pragma unroll
-        for (int u = 0; u < kScanB; ++u)
-            if (t0 + u < nt) v[u] = E[base + (long long)(t0 + u) * nlines];
-#pragma unroll
-        for (int u = 0; u < kScanB; ++u)
-            if (t0 + u < nt) {
-                E[base + (long long)(t0 + u) * nlines] = c;
-                c = cadd(cmul(zl[t0 + u], c), v[u]);
+            for (int u = 0; u < kScanB; ++u) {
+                const int t = dir ? nt - 1 - (i0 + u) : i0 + u;
+                if (i0 + u < nt) v[u] = A[base + (long long)t * nlines];
             }
-    }
-    const float2 s_tail = c;
-    c = f2(0.f, 0.f);
-    for (int t1 = nt - 1; t1 >= 0; t1 -= kScanB) {
-        float2 v[kScanB];
 #pragma unroll
-        for (int u = 0; u < kScanB; ++u)
-            if (t1 - u >= 0) v[u] = B[base + (long long)(t1 - u) * nlines];
-#pragma unroll
-        for (int u = 0; u < kScanB; ++u)
-            if (t1 - u >= 0) {
-                B[base + (long long)(t1 - u) * nlines] = c;
-                c = cadd(cmul(zl[t1 - u], c), v[u]);
+            for (int u = 0; u < kScanB; ++u) {
+                const int t = dir ? nt - 1 - (i0 + u) : i0 + u;
+                if (i0 + u < nt) {
+                    A[base + (long long)t * nlines] = c;
+                    c = cadd(cmul(zl[t], c), v[u]);
+                }
             }
+        }
     }
-    const float2 s_head = c;
+    fin[dir][threadIdx.x & 127] = c;   // dir 0: S_tail, dir 1: S_head
+    __syncthreads();
+    if (dir || !live) return;
+    const float2 s_tail = c, s_head = fin[1][threadIdx.x];
     const float2 zn = j ? f2(ax.znr[1], ax.zni[1]) : f2(ax.znr[0], ax.zni[0]);   // no dynamic param indexing
     const float2 inv = j ? f2(ax.invr[1], ax.invi[1]) : f2(ax.invr[0], ax.invi[0]);
     const float2 um1 = cmul(cadd(s_head, cmul(zn, s_tail)), inv);
@@ -372,7 +371,7 @@ cudaError_t launch_tile(const RecTArgs &a, int groups, cudaStream_t s) {
 cudaError_t launch_scan(float2 *E, float2 *B, float4 *UV, const RecTabs &tb, const RecAxis &ax, int nt, int nlines,
                         long long nq, cudaStream_t s) {
     const long long n = nq * 2 * nlines;
-    rect_scan_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(E, B, UV, tb, ax, nt, nlines, n);
+    rect_scan_kernel<<<(unsigned)((n + 127) / 128), 256, 0, s>>>(E, B, UV, tb, ax, nt, nlines, n);
     return cudaGetLastError();
 }
 
