@@ -142,58 +142,77 @@ __device__ __forceinline__ void summaries(const float4 *zp, int n, X xat, St &e,
     }
 }
 
-// exact blur of one pair along a segment from its entering states: r0/r1[m * stride] (the two
-// planes) <- sum_j Re[A_j (u_j + v_j)] - g0 x
+// exact blur of one pair along a segment from its entering states: r0/r1[m] (the two planes)
+// <- sum_j Re[A_j (u_j + v_j)] - g0 x. Full segments run the causal step at m = i and the
+// anticausal one at m = T-1-i in the same iteration (two independent chains); the first half of
+// the iterations stores, the second half (where the other direction already wrote) adds.
 template <bool FULL, class X>
 __device__ __forceinline__ void blur_segment(const RecAxis &ax, int n, X xat, const St &l, const St &r, float *r0,
                                              float *r1) {
-    St st = l;
-#pragma unroll 8
-    for (int m = 0; m < T; ++m) {
-        if (FULL || m < n) {
+    St sf = l, sb = r;
+    if constexpr (FULL) {
+#pragma unroll 4
+        for (int i = 0; i < T / 2; ++i) {
+            const int mb = T - 1 - i;
+            const float2 xf = xat(i), xb = xat(mb);
+            step(ax, sf, xf);
+            step(ax, sb, xb);
+            const float2 yf = fma2s(-ax.g0, xf, re_a(ax, sf));
+            const float2 yb = re_a(ax, sb);
+            r0[i] = yf.x;
+            r1[i] = yf.y;
+            r0[mb] = yb.x;
+            r1[mb] = yb.y;
+        }
+#pragma unroll 4
+        for (int i = T / 2; i < T; ++i) {
+            const int mb = T - 1 - i;
+            const float2 xf = xat(i), xb = xat(mb);
+            step(ax, sf, xf);
+            step(ax, sb, xb);
+            const float2 yf = fma2s(-ax.g0, xf, re_a(ax, sf));
+            const float2 yb = re_a(ax, sb);
+            r0[i] += yf.x;
+            r1[i] += yf.y;
+            r0[mb] += yb.x;
+            r1[mb] += yb.y;
+        }
+    } else {
+        for (int m = 0; m < n; ++m) {
             const float2 x = xat(m);
-            step(ax, st, x);
-            const float2 yv = fma2s(-ax.g0, x, re_a(ax, st));
+            step(ax, sf, x);
+            const float2 yv = fma2s(-ax.g0, x, re_a(ax, sf));
             r0[m] = yv.x;
             r1[m] = yv.y;
         }
-    }
-    st = r;
-#pragma unroll 8
-    for (int m = T - 1; m >= 0; --m) {
-        if (FULL || m < n) {
-            step(ax, st, xat(m));
-            const float2 v = re_a(ax, st);
+        for (int m = n - 1; m >= 0; --m) {
+            step(ax, sb, xat(m));
+            const float2 v = re_a(ax, sb);
             r0[m] += v.x;
             r1[m] += v.y;
         }
     }
 }
 
-// exact column blur of one pair, folded into acc[m * 32] += Re[conj(H) blur] (Alg. 1);
-// acc is this thread's column of the group's shared-memory accumulator
+// exact column blur of one pair, folded into acc[m * T] += Re[conj(H) blur] (Alg. 1);
+// acc is this thread's column of the group's shared-memory accumulator. Both directions in the
+// same iteration (independent chains; the accumulation is a sum, so the order is free).
 template <bool FULL>
 __device__ __forceinline__ void blur_accumulate(const RecAxis &ax, int n, const float *c0, const float *c1,
                                                 const float2 *h, const St &l, const St &r, float *acc) {
-    St st = l;
-#pragma unroll 8
-    for (int m = 0; m < T; ++m) {
-        if (FULL || m < n) {
-            const float2 xv = f2(c0[m * TP], c1[m * TP]);
-            step(ax, st, xv);
-            const float2 yv = fma2s(-ax.g0, xv, re_a(ax, st));
-            const float2 hm = h[m * TP];
-            acc[m * T] = fmaf(hm.x, yv.x, fmaf(hm.y, yv.y, acc[m * T]));
-        }
-    }
-    st = r;
-#pragma unroll 8
-    for (int m = T - 1; m >= 0; --m) {
-        if (FULL || m < n) {
-            step(ax, st, f2(c0[m * TP], c1[m * TP]));
-            const float2 v = re_a(ax, st);
-            const float2 hm = h[m * TP];
-            acc[m * T] = fmaf(hm.x, v.x, fmaf(hm.y, v.y, acc[m * T]));
+    St sf = l, sb = r;
+#pragma unroll 4
+    for (int i = 0; i < T; ++i) {
+        if (FULL || i < n) {
+            const int mb = (FULL ? T : n) - 1 - i;
+            const float2 xf = f2(c0[i * TP], c1[i * TP]), xb = f2(c0[mb * TP], c1[mb * TP]);
+            step(ax, sf, xf);
+            step(ax, sb, xb);
+            const float2 yf = fma2s(-ax.g0, xf, re_a(ax, sf));
+            const float2 yb = re_a(ax, sb);
+            const float2 hf = h[i * TP], hb = h[mb * TP];
+            acc[i * T] = fmaf(hf.x, yf.x, fmaf(hf.y, yf.y, acc[i * T]));
+            acc[mb * T] = fmaf(hb.x, yb.x, fmaf(hb.y, yb.y, acc[mb * T]));
         }
     }
 }
@@ -235,16 +254,15 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
         return f2(h.x * fv, h.y * fv);
     };
 
+    // entering states, software-pipelined: the row states of sample b are loaded during sample
+    // b-1's column stage, the column states of sample b during its row stage
+    St rl, rr, cl, cr;
+    if (MODE >= 1 && s0 < s1 && lane < Ly) get_states(a.Eh, a.Bh, a.UVh, a.th, s0, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
     for (int b = s0; b < s1; ++b) {
         const int k = a.k0 + b;
         float tk[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) tk[c] = a.t[(long long)k * D + c];
-        St rl, rr, cl, cr;
-        if (MODE >= 1 && lane < Ly)   // issued before the modulation; used by the row stage
-            get_states(a.Eh, a.Bh, a.UVh, a.th, b, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
-        if (MODE == 2 && lane < Lx)   // the column stage's, in flight during the row stage
-            get_states(a.Ev, a.Bv, a.UVv, a.tv, b, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
         __syncthreads();   // the previous sample's stages are done with cs / rb (and fs is complete)
         for (int e = tid; e < T * T; e += 32 * NP) {
             const int i = e / T, j = e % T;
@@ -259,6 +277,7 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
 
         // ---- row stage: lane = row ----
         const bool full = Lx == T && Ly == T;
+        if (MODE == 2 && lane < Lx) get_states(a.Ev, a.Bv, a.UVv, a.tv, b, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
         if (lane < Ly) {
             const float2 *hrow = cs + lane * TP;
             const float *frow = fs + ((p > 0 ? p - 1 : 0) * T + lane) * TP;
@@ -282,6 +301,8 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
             }
         }
         if (MODE == 0) continue;
+        if (b + 1 < s1 && lane < Ly)
+            get_states(a.Eh, a.Bh, a.UVh, a.th, b + 1, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
         __syncthreads();
 
         // ---- column stage: lane = column ----
