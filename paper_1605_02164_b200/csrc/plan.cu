@@ -230,6 +230,7 @@ bf_status_t ensure_pz(bf_vec_plan_t p, size_t bytes) {
     p->dpz = nullptr;
     p->pz_bytes = 0;
     BF_CUDA(cudaMalloc(&p->dpz, bytes));
+    p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
     p->pz_bytes = bytes;
     return BF_OK;
 }
@@ -247,6 +248,7 @@ bf_status_t to_lab(bf_vec_plan_t p, const float *f, int rows, const float **out,
         p->dlab = nullptr;
         p->dlab_bytes = 0;
         BF_CUDA(cudaMalloc(&p->dlab, bytes));
+        p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
         p->dlab_bytes = bytes;
     }
     BF_CUDA(launch_srgb_to_lab(f, p->dlab, (long long)rows * p->W, s));
@@ -327,6 +329,7 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
         p->dfpad = nullptr;
         p->fpad_bytes = 0;
         BF_CUDA(cudaMalloc(&p->dfpad, fbytes));
+        p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
         p->fpad_bytes = fbytes;
     }
     fill_mu(p);
@@ -458,6 +461,7 @@ bf_status_t ensure_rec_scratch(bf_vec_plan_t p, int nb) {
         p->drec = nullptr;
         p->drec_bytes = 0;
         BF_CUDA(cudaMalloc(&p->drec, 2 * per * nb));
+        p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
         p->drec_bytes = 2 * per * nb;
     }
     return BF_OK;
@@ -492,6 +496,7 @@ bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
         p->drtab = nullptr;
         p->drtab_n = 0;
         BF_CUDA(cudaMalloc(&p->drtab, sizeof(float2) * n));
+        p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
         BF_CUDA(cudaMemcpy(p->drtab, h.data(), sizeof(float2) * n, cudaMemcpyHostToDevice));
         p->drtab_n = n;
     }
@@ -527,6 +532,7 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
         p->drec = nullptr;
         p->drec_bytes = 0;
         BF_CUDA(cudaMalloc(&p->drec, per * nb));
+        p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
         p->drec_bytes = per * nb;
     }
     bf_status_t st = ensure_pz(p, sizeof(float) * (size_t)g * (p->d + 1) * px);
@@ -802,8 +808,10 @@ bf_status_t filter_graph(bf_vec_plan_t p, const float *f, float *out, cudaStream
     const bool key_seen = p->g_f == f && p->g_out == out && p->g_stream == s && p->g_gen == p->gen;
     if (!key_seen) {   // first call with this key: eager, remember the key
         if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
-        p->g_f = f; p->g_out = out; p->g_stream = s; p->g_gen = p->gen;
-        return filter_band(p, f, p->H, 0, 0, p->H, out, s);
+        p->g_f = f; p->g_out = out; p->g_stream = s;
+        const bf_status_t st = filter_band(p, f, p->H, 0, 0, p->H, out, s);
+        p->g_gen = p->gen;   // after the call: its scratch allocations bump gen
+        return st;
     }
     // second call: capture (profiling events stay outside the graph)
     const bool prof = p->profile;

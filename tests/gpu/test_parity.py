@@ -278,6 +278,22 @@ def test_graph_replay_bitwise_equals_eager():
     p.set_option("graph", 0)
     box = p.filter(f).clone()
     assert torch.equal(out, box)
+    # another entry point that grows the plan's scratch (partial planes of 4 images) frees the
+    # buffers the captured graph points at: the next call must re-capture, not replay stale pointers
+    p.set_option("graph", 1)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            p.filter(f, out)
+    s.synchronize()
+    assert p.info("graph_ready") == 1
+    p.filter_batch(torch.stack([f] * 4))
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            out.zero_()
+            p.filter(f, out)
+    s.synchronize()
+    assert torch.equal(out, box)
 
 
 @pytest.mark.parametrize("case", [(3, 64, 64, 3, 2.0, 20, 32), (5, 37, 45, 3, 5.0, 30, 9), (2, 96, 64, 8, 3.0, 20, 6),
