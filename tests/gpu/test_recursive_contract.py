@@ -12,7 +12,6 @@ import numpy as np
 import pytest
 import torch
 
-from paper_1605_02164_b200 import Plan
 from workloads.configs import random_image
 
 pytestmark = pytest.mark.gpu
@@ -21,6 +20,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("rec_impl", [1, 0])
 @pytest.mark.parametrize("sigma_s", [2.0, 5.0, 10.0])
 def test_recursive_blur_within_half_intensity_of_fir(sigma_s, rec_impl):
+    from paper_1605_02164_b200 import Plan
     H = W = 256
     f_np = random_image(H, W, 3, seed=int(sigma_s) + 40)
     f = torch.from_numpy(f_np).cuda()
@@ -57,6 +57,7 @@ def _median_ms(p, f, out, reps=9):
 
 @pytest.mark.parametrize("rec_impl", [1, 0])
 def test_recursive_runtime_independent_of_sigma(rec_impl):
+    from paper_1605_02164_b200 import Plan
     H = W = 512
     f = torch.from_numpy(random_image(H, W, 3, seed=3)).cuda()
     out = torch.empty_like(f)
