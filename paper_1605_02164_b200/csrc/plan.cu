@@ -521,7 +521,10 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     const size_t uv_h = (size_t)NQ * 2 * p->H, uv_v = (size_t)NQ * 2 * p->W;
     const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v);
     const size_t free_b = free_memory(p);
-    int nb = (int)std::max(1.0, std::min<double>(256.0, 0.4 * (double)free_b / (double)per));
+    // batch: up to 256 samples within 40 % of the free memory, but no more than 16 samples or 4 GiB
+    // of summaries (whichever allows more) -- a larger batch only saves launches (5 per batch)
+    const double cap = std::max(16.0, 4.0 * 1024 * 1024 * 1024 / (double)per);
+    int nb = (int)std::max(1.0, std::min({256.0, 0.4 * (double)free_b / (double)per, cap}));
     if (p->force_batch > 0) nb = p->force_batch;
     nb = std::min(nb, ns);
     // sample groups: enough CTAs for ~8 per SM where the tile count alone does not give them

@@ -4,7 +4,7 @@ echo "pytest exit $?"
 for impl in 1; do
   for s in 2 16 64; do
     echo "impl=$impl sigma=$s" >> gpurun_out/rec59.txt
-    timeout 300 python tools/profile_run.py --config 5 --engine 1 --rec-impl $impl --sigma $s --samples 28 --reps 3 >> gpurun_out/rec59.txt 2>&1
+    timeout 300 python tools/profile_run.py --config 5 --engine 1 --rec-impl $impl --sigma $s --samples 28 --reps 5 >> gpurun_out/rec59.txt 2>&1
   done
 done
 echo "sweep exit $?"
