@@ -272,10 +272,10 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 planes stay in shared memory; 0 staged -- a row pass and a
  *                 column pass through HBM scratch. Same arithmetic, results equal to fp32
  *                 rounding (both gated against the oracle).
- *   "rec_batch"   engine 1: samples per batch (0 = auto from free device memory; at most 256
- *                 and 40 % of the free device memory; each sample in flight holds, staged,
- *                 5 (d+1) fp32 planes of H x W scratch, tiled, 16 (d+1) fp32 values per 32
- *                 pixels of each axis' lines)
+ *   "rec_batch"   engine 1: samples per batch (0 = auto: at most 256 and 40 % of the free
+ *                 device memory, and for the tiled engine at most max(16 samples, 4 GiB of
+ *                 summaries); each sample in flight holds, staged, 5 (d+1) fp32 planes of H x W
+ *                 scratch, tiled, 16 (d+1) fp32 values per 32 pixels of each axis' lines)
  *   "spatial_kernel" separable spatial taps on the window [-r, r], r = ceil(3 sigma_s):
  *                 0 Gaussian of Eq. (1) (default), 1 box w(m) = 1, 2 hat w(m) = r + 1 - |m|
  *                 ("any arbitrary spatial filter (such as a box or hat filter)";
