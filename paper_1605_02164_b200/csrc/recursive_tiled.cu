@@ -303,7 +303,9 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
         if (MODE == 0) continue;
         if (b + 1 < s1 && lane < Ly)
             get_states(a.Eh, a.Bh, a.UVh, a.th, b + 1, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
-        __syncthreads();
+        // the column stage of pair p reads only rb planes 2p, 2p+1 (written by this warp) and cs
+        // (complete since the barrier after the modulation): a warp barrier suffices
+        __syncwarp();
 
         // ---- column stage: lane = column ----
         if (lane < Lx) {
