@@ -10,7 +10,7 @@ namespace bfvec {
 
 #define BFV_INSTANCES(X) X(3, 2, 128, 16, 16) X(3, 4, 128, 16, 16) X(3, 6, 128, 16, 16) X(3, 10, 128, 16, 16) X(3, 15, 128, 16, 16) X(3, 24, 256, 16, 16) X(3, 30, 256, 16, 16) X(3, 48, 256, 16, 16) X(3, 64, 64, 8, 8)
 #define BFV_TMEM_INSTANCES(X) X(3, 2) X(3, 4) X(3, 6) X(3, 10) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
-#define BFV_TMEM2_INSTANCES(X) X(3, 6) X(3, 10) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
+#define BFV_TMEM2_INSTANCES(X) X(3, 3) X(3, 6) X(3, 10) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
 
 // variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 3 v4 with two
 // consumer warps per pair (R = 48), 4 force v5 (two samples per pass, two consumer
