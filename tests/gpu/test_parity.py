@@ -95,6 +95,9 @@ EDGE = [
     (90, 64, 4, 16.0, 40, 3, 13, "diag"),     # d = 4, r = 48 (v3)
     (64, 64, 3, 16.0, 40, 3, 14, "full"),     # r = 48 default kernel (v5): one sample pair + a one-sample tail
     (64, 64, 3, 10.0, 40, 2, 15, "full"),     # v5 at r = 30 with a single pass
+    (77, 100, 3, 1.0, 10, 7, 16, "full"),     # two-sample kernel at R = 3 (d = 3): several strips, odd M
+    (45, 70, 1, 2.0, 16, 5, 17, "diag"),      # two-sample kernel at R = 6, d = 1
+    (60, 50, 2, 3.3, 20, 6, 18, "full"),      # two-sample kernel at R = 10, d = 2
 ]
 
 
