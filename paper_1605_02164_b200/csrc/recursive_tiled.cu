@@ -17,8 +17,13 @@
 //   pass 1 (tile)  : exact row blur of the tile into shared memory, column summaries
 //   scan columns   : the same along columns
 //   pass 2 (tile)  : exact row blur, exact column blur, Re[conj(H) blur] (Alg. 1) summed
-//                    over the group's samples in registers, one partial plane set per group.
+//                    over the group's samples in a shared-memory accumulator, one partial plane
+//                    set per group.
 // HBM sees f, the summaries (8 B per pixel-sample per axis) and the partial sums only.
+// Inside a tile: summaries are dot products with z^m (no dependency chain); an exact segment
+// runs its causal and anticausal recursions interleaved (two independent chains); the entering
+// states are loaded one stage ahead; each warp owns one (cos, sin) pair of planes, so only the
+// modulation needs a CTA barrier.
 #include <cuda_runtime.h>
 
 #include "internal.h"
