@@ -242,11 +242,13 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 1 shared-memory ring (v3), 2 tensor-memory ring (v4, d <= 3), 3 v4 with two
  *                 consumer warps per (cos, sin) pair (d <= 3, r in (30, 48]), 4 v6: tensor-
  *                 memory double ring, two samples per pass, two consumer warps per pair,
- *                 four dedicated modulation warps (d <= 3, r in (10, 48]), 5 v5 with one
- *                 consumer warp per pair, 6 v5c (v6 without the modulation warps) (both
- *                 d = 3, r in (30, 48]), 7 v6 with running-sum FIRs for box taps (d = 3,
- *                 spatial_kernel = 1, r in {15, 24, 30, 48}; chosen automatically for box
- *                 taps); a variant not compiled for the plan falls back to the default order
+ *                 four dedicated modulation warps (d <= 3, r <= 48 where an instance fits), 5
+ *                 v5 with one consumer warp per pair, 6 v5c (v6 without the modulation warps)
+ *                 (both d = 3, r in (30, 48]), 7 v6 with running-sum FIRs for box taps (d = 3,
+ *                 spatial_kernel = 1, r equal to a compiled radius; chosen automatically for box
+ *                 taps), 8 tensor-memory ring for 5 <= d <= 8 (three launches per call: pairs
+ *                 {Z, P0..P2}, {P3..P6}, then P7 for four samples at once; r <= 24); a variant
+ *                 not compiled for the plan falls back to the default order
  *   "engine"      how Alg. 1 step 10 convolves: 0 (default) the truncated
  *                 separable window [-r, r] of Eq. (1) / "spatial_kernel", O(r) per pixel-sample
  *                 (fused sm_100a kernel); 1 the recursive O(1)-in-sigma_s engine of PAPER.md:204

@@ -1192,7 +1192,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
     if (!std::strcmp(name, "tile_rows")) { if (v < 0) return BF_E_ARG; p->force_tile_rows = (int)v; return BF_OK; }
     if (!std::strcmp(name, "groups")) { if (v < 0) return BF_E_ARG; p->force_groups = (int)v; return BF_OK; }
     if (!std::strcmp(name, "variant")) {
-        if (v < 0 || v > 7) return BF_E_ARG;
+        if (v < 0 || v > 8) return BF_E_ARG;
         p->force_variant = (int)v;
         if (p->device >= 0) {   // re-select the kernel instance
             if (!select_kernel(p)) return BF_E_UNSUPPORTED;

@@ -44,3 +44,40 @@ def test_edge_parity(variant, case):
         res = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
         print(variant, case, tr, g, res)
         H.assert_gates(res)
+
+
+# variant 8: the tensor-memory ring for 5 <= d <= 8 (three launches: {Z, P0..P2}, {P3..P6}, P7 for
+# four samples at once). Sample counts that leave the last four-sample pass partly empty (5, 7, 9),
+# ragged tiles, d = 5 (channels 5..7 zero), forced schedules.
+@pytest.mark.parametrize("case", [(96, 70, 8, 8.0, 30, 9, 12, "full"), (64, 96, 8, 2.0, 30, 7, 7, "diag"),
+                                  (29, 66, 5, 1.0, 12, 5, 6, "full"), (50, 41, 6, 5.0, 20, 6, 3, "diag")])
+def test_variant8_edge_parity(case):
+    cfg = _edge_cfg(case)
+    f = random_image(cfg.H, cfg.W, cfg.d, seed=cfg.seed, smooth=True)
+    Q, a, Y = H.oracle_draws(cfg)
+    S_o, P_o, Z_o = native.mcsf_full(f, Q, a, cfg.N, Y, cfg.sigma_s)
+    p = H.gpu_plan(cfg)
+    p.set_option("variant", 8)
+    assert p.info("variant") == 8
+    for tr, g in [(0, 0), (32, 2), (48, 3)]:
+        p.set_option("tile_rows", tr)
+        p.set_option("groups", g)
+        res = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
+        print(case, tr, g, res)
+        H.assert_gates(res)
+
+
+def test_variant8_config4_bands():
+    """Config 4 at full size with variant 8, checked on two row bands against the oracle."""
+    cfg = CONFIGS[4]
+    f = make_image(cfg)
+    Q, a, Y = H.oracle_draws(cfg)
+    p = H.gpu_plan(cfg)
+    p.set_option("variant", 8)
+    S_g, P_g, Z_g = H.gpu_run(p, f)
+    get_rows = lambda y0, y1: f[:, y0:y1]
+    for y0 in (0, cfg.H - 16):
+        S_o, P_o, Z_o = H.oracle_band(cfg, get_rows, Q, a, Y, y0, 16)
+        res = H.gates(cfg, S_g[:, y0:y0 + 16], P_g[:, y0:y0 + 16], Z_g[y0:y0 + 16], S_o, P_o, Z_o)
+        print("config 4 variant 8 band", y0, res)
+        H.assert_gates(res)
