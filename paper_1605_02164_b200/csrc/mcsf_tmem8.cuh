@@ -263,29 +263,26 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
                 // KIND 2: rows of the chunk this warp reduces over the four slots and writes
                 constexpr int RW = C::KB / (C::NB / 32);
                 const int rr0 = wi * RW;
+                // the old partial sums this thread read-modify-writes in chunk (first, cy), loaded one
+                // chunk ahead so their latency overlaps the previous chunk's FIR
+                constexpr int NO = (C::KIND == 2) ? RW : OR;
+                const int orow = (C::KIND == 2) ? rr0 : H0;
+                const long long opl = (C::KIND == 2) ? 7 : pl;
+                auto load_old = [&](float (&o_)[NO], int cy, bool first) {
+#pragma unroll
+                    for (int o = 0; o < NO; ++o) {
+                        const bool ok = xok && (cy + orow + o < ty1);
+                        o_[o] = (!first && ok) ? pzb[opl * plane_out + (long long)(cy + orow + o - a.out_row0) * a.W]
+                                               : 0.f;
+                    }
+                };
+                float old[NO];
+                load_old(old, ty0, true);
                 int q = 0;
                 for (int k = gk0, pass = 0; k < gk1; k += C::NS, ++pass) {
-                    const bool first_k = (k == gk0);
                     const int gs = pass * rows_per_pass;
                     for (int ci = 0; ci < nchunks; ++ci, ++q) {
                         const int cy = ty0 + ci * C::KB;
-                        float old[C::KIND == 2 ? RW : OR];
-                        if constexpr (C::KIND == 2) {
-#pragma unroll
-                            for (int o = 0; o < RW; ++o) {
-                                const bool ok = xok && (cy + rr0 + o < ty1);
-                                old[o] = (!first_k && ok)
-                                             ? pzb[7 * plane_out + (long long)(cy + rr0 + o - a.out_row0) * a.W]
-                                             : 0.f;
-                            }
-                        } else {
-#pragma unroll
-                            for (int o = 0; o < OR; ++o) {
-                                const bool ok = xok && (cy + H0 + o < ty1);
-                                old[o] = (!first_k && ok) ? pzb[pl * plane_out + (long long)(cy + H0 + o - a.out_row0) * a.W]
-                                                          : 0.f;
-                            }
-                        }
                         mbar_wait(&full[q & 1], (q >> 1) & 1);
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         float2 acc[OR];
@@ -352,6 +349,9 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
                                         dst[(long long)o * a.W] = fmaf(cs[o].x, acc[o].x, fmaf(cs[o].y, acc[o].y, old[o]));
                             }
                         }
+                        // next chunk: the next 16 rows of this pass, or the first rows of the next pass
+                        if (ci + 1 < nchunks) load_old(old, cy + C::KB, k == gk0);   // first pass: initialise
+                        else if (k + C::NS < gk1) load_old(old, ty0, false);
                     }
                 }
             };
