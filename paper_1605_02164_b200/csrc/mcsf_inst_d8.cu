@@ -9,11 +9,13 @@ namespace bfvec {
 // sub-step (9 pairs x 8 rows x 4 groups); 14 % faster on config 4 than NA = 96
 #define BFV_INSTANCES(X) X(8, 6, 288, 16, 8) X(8, 15, 288, 16, 8) X(8, 24, 288, 8, 8)
 // tensor-memory ring, three launches per call (mcsf_tmem8.cuh)
-#define BFV_TMEM8_INSTANCES(X) X(24)
+#define BFV_TMEM8_INSTANCES(X) X(6) X(15) X(24)
 
-// variant 0: auto (v3 for now), 1: v3 (shared-memory ring), 8: tensor-memory ring
+// variant 0: auto (the tensor-memory ring where an instance fits: 1.08x / 1.07x the shared-memory
+// ring at r = 6 / 24, equal at r = 15, profiles/r01_v8_vs_v3.txt), 1: v3 (shared-memory ring),
+// 8: tensor-memory ring
 bool fused_select_d8(int r, int variant, KernelInfo *info) {
-    if (variant == 8) {
+    if (variant == 8 || variant == 0) {
         int best8 = 1 << 30;
 #define BFV_PICK8(R_) \
     if (R_ >= r && R_ < best8) best8 = R_;

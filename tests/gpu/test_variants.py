@@ -81,3 +81,18 @@ def test_variant8_config4_bands():
         res = H.gates(cfg, S_g[:, y0:y0 + 16], P_g[:, y0:y0 + 16], Z_g[y0:y0 + 16], S_o, P_o, Z_o)
         print("config 4 variant 8 band", y0, res)
         H.assert_gates(res)
+
+
+@pytest.mark.parametrize("case", [(96, 70, 8, 8.0, 30, 9, 12, "full"), (29, 66, 5, 1.0, 12, 5, 6, "full")])
+def test_variant1_d8_parity(case):
+    """The shared-memory-ring kernel (variant 1) for d = 8, no longer the default there."""
+    cfg = _edge_cfg(case)
+    f = random_image(cfg.H, cfg.W, cfg.d, seed=cfg.seed, smooth=True)
+    Q, a, Y = H.oracle_draws(cfg)
+    S_o, P_o, Z_o = native.mcsf_full(f, Q, a, cfg.N, Y, cfg.sigma_s)
+    p = H.gpu_plan(cfg)
+    p.set_option("variant", 1)
+    assert p.info("variant") == 1
+    res = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
+    print(case, res)
+    H.assert_gates(res)
