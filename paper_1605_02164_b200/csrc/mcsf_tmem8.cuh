@@ -157,6 +157,9 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = *taddr_s;
+    // let the next launch of the call start on SMs this one frees (its CTAs only begin once every
+    // CTA of this grid has started; it writes other planes)
+    if (C::KIND < 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (gk0 < gk1) {
         if (tid < C::NA) {
@@ -368,6 +371,10 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(C::TCOLS) : "memory");
+    // launches 1 and 2 start early (programmatic stream serialisation) to fill the previous
+    // launch's last wave; they touch other partial planes, but a grid may only COMPLETE after its
+    // predecessor, so whatever follows on the stream (normalise) sees all three launches done
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 template <class C>
@@ -376,8 +383,21 @@ cudaError_t launch_tmem8_one(const FusedArgs &a, dim3 grid, cudaStream_t s) {
     static std::atomic<uint64_t> attr{0};
     const cudaError_t e = ensure_smem_attr(k, C::SMEM, attr);
     if (e != cudaSuccess) return e;
-    k<<<grid, C::NT, C::SMEM, s>>>(a);
-    return cudaGetLastError();
+    if (C::KIND == 0) {
+        k<<<grid, C::NT, C::SMEM, s>>>(a);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(C::NT);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, a);
 }
 
 // the three launches of one filter call (KIND 0, 1, 2: disjoint partial planes of the same groups)
