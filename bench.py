@@ -142,7 +142,7 @@ def recursive_flops_per_px_sample(d):
 
 KERNEL_NAMES = {1: "mcsf_fused_kernel", 2: "mcsf_tmem_kernel", 3: "mcsf_tmem_kernel(CW=2)", 4: "mcsf_tmem2_kernel",
                 5: "mcsf_tmem2_kernel(CW=1)", 6: "mcsf_tmem2_kernel(MW=0)", 7: "mcsf_tmem2_kernel(box)",
-                8: "mcsf_tmem8_kernel x3"}
+                8: "mcsf_tmem8_kernel x2"}
 
 
 def measured_traffic(cfg, kernel, units, schedule):

@@ -247,8 +247,8 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 v5 with one consumer warp per pair, 6 v5c (v6 without the modulation warps)
  *                 (both d = 3, r in (30, 48]), 7 v6 with running-sum FIRs for box taps (d = 3,
  *                 spatial_kernel = 1, r equal to a compiled radius; chosen automatically for box
- *                 taps), 8 tensor-memory ring for 5 <= d <= 8 (three launches per call: pairs
- *                 {Z, P0..P2}, {P3..P6}, then P7 for four samples at once; r <= 24); a variant
+ *                 taps), 8 tensor-memory ring for 5 <= d <= 8 (two launches per call: pairs
+ *                 {Z, P0..P6} two per TMEM quarter, then P7 for four samples at once; r <= 24); a variant
  *                 not compiled for the plan falls back to the default order
  *   "engine"      how Alg. 1 step 10 convolves: 0 (default) the truncated
  *                 separable window [-r, r] of Eq. (1) / "spatial_kernel", O(r) per pixel-sample

@@ -1,23 +1,23 @@
 // mcsf_tmem8.cuh -- the tensor-memory-ring kernel for 8-channel images (variant 8; d = 5 .. 8).
 //
-// The TMEM kernels give every (cos, sin) pair of planes one TMEM lane quarter, i.e. one SM
+// The TMEM kernels give every (cos, sin) pair of planes a TMEM lane quarter, i.e. an SM
 // sub-partition (a warp reaches only the quarter warp_id % 4). Eight channels have nine pairs:
 // Z, P_0 .. P_7 (Alg. 1, G_t = H_t f), which do not spread evenly over four
-// quarters. So one filter call is three launches of this kernel, each filling all four quarters:
-//   KIND 0: pairs {Z, P_0, P_1, P_2} of one sample per pass,
-//   KIND 1: pairs {P_3, P_4, P_5, P_6} of one sample per pass,
+// quarters. So one filter call is two launches of this kernel, each filling all four quarters:
+//   KIND 3: the eight pairs {Z, P_0 .. P_6}, two per quarter (TMEM column blocks 0 and 1), one
+//           producer and one consumer warp per pair, one modulation per pixel for all eight,
 //   KIND 2: pair P_7 of FOUR samples per pass (quarter q <- sample k + q); the four quarters'
 //           Re[conj(H) blur] (Alg. 1) are summed through shared memory before the one
 //           read-modify-write of the P_7 partial plane.
 // 9/8 of a four-pair pass per sample in total, all quarters busy; the phase t_k . f (Alg. 1)
-// needs all eight channels in every launch, so the sincos is computed three times per
-// pixel-sample (SFU, small next to the FIR).
+// needs all eight channels in both launches. (KIND 0 / 1 -- {Z, P_0 .. P_2} and {P_3 .. P_6} in two
+// launches -- were the first version: the 8-channel modulation, done twice per pixel, bound them.)
 //
 // Otherwise the dataflow of v4 (mcsf_tmem.cuh): producer warps stage f by TMA (8 floats per
-// padded pixel), modulate into double-buffered G-pairs in shared memory, run the horizontal FIR
-// with FFMA2 (Alg. 1) and hand rows to the TMEM ring (transpose through a per-warp tile,
-// tcgen05.st); consumer warps read 16-row TMEM blocks (tcgen05.ld), run the vertical FIR and
-// accumulate. Row bookkeeping as in v4.
+// padded pixel), modulate into G-pairs in shared memory, run the horizontal FIR with FFMA2
+// (Alg. 1) and hand rows to the TMEM ring (transpose through a per-warp tile, tcgen05.st);
+// consumer warps read 16-row TMEM blocks (tcgen05.ld), run the vertical FIR and accumulate. Row
+// bookkeeping as in v4.
 #pragma once
 #include "mcsf_tmem.cuh"
 
@@ -32,12 +32,16 @@ struct CfgT8 {
     static constexpr int KB = 16;
     static constexpr int SH = 16;
     static constexpr int TX = kTX;
-    static constexpr int NQ = 4;             // slots = TMEM lane quarters
+    // KIND 3: the eight pairs {Z, P_0 .. P_6} in ONE launch, two per TMEM quarter (column blocks
+    // 0 and 1), one modulation per pixel for all eight; slots 0..3 otherwise
+    static constexpr int NQ = (KIND_ == 3) ? 8 : 4;
     static constexpr int NS = (KIND_ == 2) ? 4 : 1;   // samples per pass
     static constexpr int NA = 256;           // producers: warp w -> slot w & 3, rows 8 (w >> 2) .. +8
-    static constexpr int CW = CW_;
-    static constexpr int OR = KB / CW_;
-    static constexpr int NB = 128 * CW_;
+                                             //   (KIND 3: slot w, both 8-row halves)
+    static constexpr int CW = (KIND_ == 3) ? 1 : CW_;
+    static constexpr int OR = KB / CW;
+    static constexpr int NB = 256;           // consumers: (slot, half) pairs, KIND 3: one warp per slot
+    static constexpr int GB = (KIND_ == 3) ? 1 : 2;   // G-pair buffers (KIND 3: one, it is 8 pairs wide)
     static constexpr int NT = NA + NB;
     static constexpr int DP = 8;
     static constexpr int WIN = TX + 2 * R;
@@ -46,15 +50,16 @@ struct CfgT8 {
     static constexpr int HROWS = A + KB;
     static constexpr int RING = A + KB - R;
     static constexpr int NIN = 8 + 2 * R;
-    static constexpr int TCOLS = (2 * HROWS <= 32) ? 32 : (2 * HROWS <= 64) ? 64 : (2 * HROWS <= 128) ? 128
-                               : (2 * HROWS <= 256) ? 256 : 512;
+    static constexpr int QCOLS = (NQ / 4) * 2 * HROWS;   // TMEM columns per quarter
+    static constexpr int TCOLS = (QCOLS <= 32) ? 32 : (QCOLS <= 64) ? 64 : (QCOLS <= 128) ? 128
+                               : (QCOLS <= 256) ? 256 : 512;
     static constexpr int SZ_F = SH * WIN * DP * 4;
     static constexpr int SZ_G = NQ * SH * MS * 8;
     static constexpr int SZ_RING = RING * TX * 8;
     static constexpr int SZ_RED = (KIND_ == 2) ? 2 * NQ * KB * TX * 4 : 0;
     static constexpr int OFF_F = 0;
     static constexpr int OFF_G = round_up(OFF_F + SZ_F, 128);
-    static constexpr int OFF_RING = round_up(OFF_G + 2 * SZ_G, 128);
+    static constexpr int OFF_RING = round_up(OFF_G + GB * SZ_G, 128);
     static constexpr int SZ_TP = (NA / 32) * TX * 9 * 8;
     static constexpr int OFF_TP = round_up(OFF_RING + NS * SZ_RING, 128);
     static constexpr int OFF_RED = round_up(OFF_TP + SZ_TP, 128);
@@ -62,12 +67,16 @@ struct CfgT8 {
     static constexpr size_t SMEM = OFF_BAR + 5 * 8 + 8;
     static constexpr uint32_t TMA_BYTES = SZ_F;
     // slot q: channel of its G pair (-1: Z), partial plane, sample offset within the pass
-    static constexpr int ch(int q) { return KIND_ == 0 ? q - 1 : KIND_ == 1 ? q + 3 : 7; }
-    static constexpr int plane(int q) { return KIND_ == 0 ? (q == 0 ? 8 : q - 1) : KIND_ == 1 ? q + 3 : 7; }
+    static constexpr int ch(int q) { return (KIND_ == 0 || KIND_ == 3) ? q - 1 : KIND_ == 1 ? q + 3 : 7; }
+    static constexpr int plane(int q) {
+        return (KIND_ == 0 || KIND_ == 3) ? (q == 0 ? 8 : q - 1) : KIND_ == 1 ? q + 3 : 7;
+    }
+    // TMEM column offset of slot q's ring within its quarter
+    static constexpr int qcol(int q) { return (q >> 2) * 2 * HROWS; }
     static constexpr int soff(int q) { return KIND_ == 2 ? q : 0; }
     static_assert(KB == 16, "one aligned 16-row block per chunk");
     static_assert(CW_ == 1 || CW_ == 2, "one or two consumer warps per slot");
-    static_assert(2 * HROWS <= 512, "TMEM columns");
+    static_assert(QCOLS <= 512, "TMEM columns");
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(WIN <= 256, "TMA box dimension");
 };
@@ -159,18 +168,17 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
     const uint32_t tbase = *taddr_s;
     // let the next launch of the call start on SMs this one frees (its CTAs only begin once every
     // CTA of this grid has started; it writes other planes)
-    if (C::KIND < 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (C::KIND != 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (gk0 < gk1) {
         if (tid < C::NA) {
             // ============================ PRODUCER ============================
             const int ta = tid;
-            const int p = warp & 3;                          // slot == TMEM quarter
-            const int rh = warp >> 2;                        // rows 8 rh .. 8 rh + 7 of a sub-step
+            const int p = (C::KIND == 3) ? warp : (warp & 3);   // slot; TMEM quarter p & 3
             const int r8 = lane & 7, cg = lane >> 3;
-            const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16);
+            const uint32_t tq = tbase + ((uint32_t)(32 * (p & 3)) << 16) + (uint32_t)C::qcol(p);
             uint32_t tparity = 0;
-            int buf = 0;
+            int buf = 0, it = 0;
             if (ta == 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0, C::TMA_BYTES);
             int q = 0;
             for (int k = gk0, pass = 0; k < gk1; k += C::NS, ++pass) {
@@ -194,9 +202,10 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const int u_begin = first_c ? 0 : C::A + (ci - 1) * C::KB;
                     const int n_new = first_c ? C::A : C::KB;
-                    for (int s0 = 0; s0 < n_new; s0 += C::SH, buf ^= 1) {
+                    for (int s0 = 0; s0 < n_new; s0 += C::SH, buf ^= 1, ++it) {
                         const int gsub = gs + u_begin + s0;
-                        float2 *gb = gbuf + buf * (C::NQ * C::SH * C::MS);
+                        float2 *gb = gbuf + (C::GB == 2 ? buf : 0) * (C::NQ * C::SH * C::MS);
+                        if (C::GB == 1 && it > 0) named_sync<C::NA>(1);   // one G buffer: previous H-pass done
                         mbar_wait(tma_bar, tparity);
                         tparity ^= 1u;
                         modulate8<C>(ta, fbuf, gb, rings, tk, act, gsub, C::SH);
@@ -209,6 +218,10 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
                             if (nu >= 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0 + nu, C::TMA_BYTES);
                         }
                         // horizontal FIR: 8 outputs (row 8 rh + r8, columns 8 cg .. 8 cg + 7) of slot p
+                        constexpr int NRH = (C::KIND == 3) ? 2 : 1;
+#pragma unroll 1
+                        for (int rr = 0; rr < NRH; ++rr) {
+                        const int rh = (C::KIND == 3) ? rr : (warp >> 2);
                         const float2 *in = gb + (p * C::SH + 8 * rh + r8) * C::MS + cg * 8;
                         float2 acc[8];
 #pragma unroll
@@ -237,6 +250,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
                         __syncwarp();
                         const int slot = (gsub + 8 * rh) % C::HROWS;
                         tmem_st16(tq + 2 * slot, acc);
+                        }
                         if (s0 + C::SH >= n_new) {
                             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -250,9 +264,9 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem8_kernel(const __grid_const
             // warp NA/32 + w: slot p = w & 3 (TMEM quarter p = warp % 4); part h = w >> 2 owns output
             // rows OR h .. OR h + OR - 1 of every chunk
             const int wi = warp - C::NA / 32;
-            const int p = warp & 3;
-            const int h = wi >> 2;
-            const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16);
+            const int p = (C::KIND == 3) ? wi : (warp & 3);   // slot; TMEM quarter warp % 4 == p & 3
+            const int h = (C::KIND == 3) ? 0 : (wi >> 2);
+            const uint32_t tq = tbase + ((uint32_t)(32 * (p & 3)) << 16) + (uint32_t)C::qcol(p);
             const int x = x0 + lane;
             const bool xok = x < a.W;
             const long long plane_out = (long long)a.out_rows * a.W;
@@ -383,7 +397,7 @@ cudaError_t launch_tmem8_one(const FusedArgs &a, dim3 grid, cudaStream_t s) {
     static std::atomic<uint64_t> attr{0};
     const cudaError_t e = ensure_smem_attr(k, C::SMEM, attr);
     if (e != cudaSuccess) return e;
-    if (C::KIND == 0) {
+    if (C::KIND == 0 || C::KIND == 3) {   // the call's first launch
         k<<<grid, C::NT, C::SMEM, s>>>(a);
         return cudaGetLastError();
     }
@@ -400,11 +414,11 @@ cudaError_t launch_tmem8_one(const FusedArgs &a, dim3 grid, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k, a);
 }
 
-// the three launches of one filter call (KIND 0, 1, 2: disjoint partial planes of the same groups)
+// the launches of one filter call (disjoint partial planes of the same groups): KIND 3 (Z, P_0 .. P_6)
+// then KIND 2 (P_7); KIND 0 / 1 split the eight pairs over two launches instead (the first version)
 template <int R>
 cudaError_t launch_tmem8(const FusedArgs &a, dim3 grid, cudaStream_t s) {
-    cudaError_t e = launch_tmem8_one<CfgT8<R, 0>>(a, grid, s);
-    if (e == cudaSuccess) e = launch_tmem8_one<CfgT8<R, 1>>(a, grid, s);
+    cudaError_t e = launch_tmem8_one<CfgT8<R, 3>>(a, grid, s);
     if (e == cudaSuccess) e = launch_tmem8_one<CfgT8<R, 2>>(a, grid, s);
     return e;
 }

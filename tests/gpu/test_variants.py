@@ -46,8 +46,8 @@ def test_edge_parity(variant, case):
         H.assert_gates(res)
 
 
-# variant 8: the tensor-memory ring for 5 <= d <= 8 (three launches: {Z, P0..P2}, {P3..P6}, P7 for
-# four samples at once). Sample counts that leave the last four-sample pass partly empty (5, 7, 9),
+# variant 8: the tensor-memory ring for 5 <= d <= 8 (two launches: {Z, P0..P6} two pairs per TMEM
+# quarter, then P7 for four samples at once). Sample counts that leave the last four-sample pass partly empty (5, 7, 9),
 # ragged tiles, d = 5 (channels 5..7 zero), forced schedules.
 @pytest.mark.parametrize("case", [(96, 70, 8, 8.0, 30, 9, 12, "full"), (64, 96, 8, 2.0, 30, 7, 7, "diag"),
                                   (29, 66, 5, 1.0, 12, 5, 6, "full"), (50, 41, 6, 5.0, 20, 6, 3, "diag")])
