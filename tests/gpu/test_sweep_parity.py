@@ -11,10 +11,11 @@ from workloads.configs import random_image, small_config
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("engine", [0, 1])
-def test_sweep_matches_oracle_curve(engine):
+@pytest.mark.parametrize("engine,d", [(0, 3), (1, 3), (0, 8)])
+def test_sweep_matches_oracle_curve(engine, d):
+    """d = 8 runs the realisation-batched sweep through the 8-channel kernel (variant 8)."""
     from paper_1605_02164_b200 import Plan
-    d, Hh, W, s, N = 3, 48, 64, 1.0, 10          # the Fig. 5 setting: sigma_s = 1, sigma_r = 30
+    Hh, W, s, N = 48, 64, 1.0, 10                # the Fig. 5 setting: sigma_s = 1, sigma_r = 30
     C = np.eye(d) * 30.0 ** 2
     cfg = small_config(d=d, H=Hh, W=W, sigma_s=s, N=N, M=64, seed=0, C=C)
     f = random_image(Hh, W, d, seed=3, smooth=True)
