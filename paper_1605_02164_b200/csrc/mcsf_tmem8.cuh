@@ -95,14 +95,32 @@ __device__ __forceinline__ void modulate8(int ta, const float *fbuf, float2 *gbu
         const float4 q0 = *reinterpret_cast<const float4 *>(fbuf + (row * C::WIN + j) * C::DP);
         const float4 q1 = *reinterpret_cast<const float4 *>(fbuf + (row * C::WIN + j) * C::DP + 4);
         const float fv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        float th[C::NS];
+        if constexpr (C::NS % 2 == 0) {   // two samples' phases per FFMA2
+#pragma unroll
+            for (int v = 0; v < C::NS / 2; ++v) {
+                float2 t2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c = 0; c < C::D; ++c)
+                    t2 = __ffma2_rn(make_float2(tk[2 * v][c], tk[2 * v + 1][c]), make_float2(fv[c], fv[c]), t2);
+                th[2 * v] = t2.x;
+                th[2 * v + 1] = t2.y;
+            }
+        } else {   // one sample: two channels per FFMA2
+#pragma unroll
+            for (int u = 0; u < C::NS; ++u) {
+                float2 t2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c = 0; c < C::D; c += 2)
+                    t2 = __ffma2_rn(make_float2(tk[u][c], tk[u][c + 1]), make_float2(fv[c], fv[c + 1]), t2);
+                th[u] = t2.x + t2.y;
+            }
+        }
         float2 cs[C::NS];
 #pragma unroll
         for (int u = 0; u < C::NS; ++u) {
-            float th = 0.f;
-#pragma unroll
-            for (int c = 0; c < C::D; ++c) th = fmaf(tk[u][c], fv[c], th);
             float s, c;
-            __sincosf(th, &s, &c);
+            __sincosf(th[u], &s, &c);
             cs[u] = act[u] ? make_float2(c, s) : make_float2(0.f, 0.f);   // inactive sample: no contribution
         }
         float2 *dst = gbuf + row * C::MS + j;
