@@ -179,11 +179,13 @@ __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0
         const bool inner = j >= C::R && j < C::R + C::TX;
         const int rs = ((g0 + row) % C::RING) * C::TX + (j - C::R);
 #pragma unroll
+        float2 th2 = make_float2(0.f, 0.f);   // both samples' phases, one FFMA2 per channel
+#pragma unroll
+        for (int c = 0; c < C::D; ++c) th2 = __ffma2_rn(make_float2(tk[0][c], tk[1][c]), make_float2(fv[c], fv[c]), th2);
+#pragma unroll
         for (int s = 0; s < 2; ++s) {
             if (s >= np) break;
-            float th = 0.f;
-#pragma unroll
-            for (int c = 0; c < C::D; ++c) th = fmaf(tk[s][c], fv[c], th);
+            const float th = s == 0 ? th2.x : th2.y;
             float sn, cn;
             __sincosf(th, &sn, &cn);
             float2 *dst = (s == 0 ? gb0 : gb1) + row * C::MS + j;
