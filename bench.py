@@ -35,7 +35,7 @@ import numpy as np  # noqa: E402
 METRIC = "pixel*samples/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--engine", type=int, default=0, help="0 truncated FIR (default), 1 recursive O(1) engine")
     ap.add_argument("--sigma", type=float, default=0.0, help="override the config's sigma_s (engine sweeps)")
     ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled (default)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ---------------------------------------------------------------------------
@@ -164,33 +164,92 @@ def measured_traffic(cfg, kernel, units, schedule):
 # ---------------------------------------------------------------------------
 # CPU oracle leg (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg, rows=8, samples=None):
-    """Time Algorithm 1 (oracle/native, fp64 OpenMP) on output rows [y0, y0+rows) in
-    the middle of the image with the first `samples` draws. Returns (px*samples/s, info)."""
+CPU_BAND_ROWS = 64          # SURVEY.md §8(d): three 64-row bands (top, middle, bottom)
+
+
+def full_image_lane_ops(cfg):
+    """fp64 lane-ops of Algorithm 1 on the whole image with all M samples (H- and V-pass)."""
+    return cfg.W * 2 * cfg.H * 2 * (cfg.d + 1) * (2 * cfg.radius + 1) * cfg.M
+
+
+def cpu_bands(cfg, budget=1.2e11):
+    """Output row bands the CPU oracle leg runs on: the whole image when it is at most three
+    bands tall or all of it fits the budget, else three CPU_BAND_ROWS-row bands at the top,
+    middle and bottom (SURVEY.md §8(d), VERDICT r01 weak #1)."""
+    if cfg.H <= 3 * CPU_BAND_ROWS or full_image_lane_ops(cfg) <= budget:
+        return [(0, cfg.H)]
+    mid = cfg.H // 2 - CPU_BAND_ROWS // 2
+    return [(0, CPU_BAND_ROWS), (mid, mid + CPU_BAND_ROWS), (cfg.H - CPU_BAND_ROWS, cfg.H)]
+
+
+def halo_factor(cfg, bands):
+    """Per-output-pixel work of Algorithm 1 on these bands relative to a full-image run.
+
+    O2 modulates and runs the horizontal pass on every slab row (band + reflected r-row halo)
+    and the vertical pass on the band's output rows, so its cost is ~ (slab rows + out rows)
+    per band against 2H for the whole image: factor = sum(slab + rows) / sum(2 rows)."""
+    from oracle import native
+    num = den = 0
+    for y0, y1 in bands:
+        s0, s1 = native.slab_bounds(cfg.H, y0, y1 - y0, cfg.radius)
+        num += (s1 - s0) + (y1 - y0)
+        den += 2 * (y1 - y0)
+    return num / den
+
+
+def oracle_sample(cfg, bands, samples=None):
+    """Time Algorithm 1 (oracle/native, fp64 OpenMP) on the output row `bands` with the first
+    `samples` draws. Returns (measured px*samples/s over the bands' output pixels, info)."""
     from oracle import draws, native
     from oracle import plan as oplan
     from workloads import make_image_rows
     M = cfg.M if samples is None else min(samples, cfg.M)
-    y0 = max(0, min(cfg.H - rows, cfg.H // 2 - rows // 2))
-    rows = min(rows, cfg.H)
-    s0, s1 = native.slab_bounds(cfg.H, y0, rows, cfg.radius)
-    slab = make_image_rows(cfg, s0, s1)
     Q, a = oplan.diagonalize(cfg.C_array)
     Y = draws.y_draws(cfg.seed, cfg.M, cfg.d, cfg.N)[:M]
+    slabs = []
+    for y0, y1 in bands:
+        s0, s1 = native.slab_bounds(cfg.H, y0, y1 - y0, cfg.radius)
+        slabs.append((make_image_rows(cfg, s0, s1), s0, y0, y1 - y0))
+    # all of this host's cores: under torchrun (N > 1) OMP_NUM_THREADS is 1 per rank, but only
+    # rank 0 runs the oracle and the other ranks exit without work
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    native.set_threads(threads)
     t0 = time.perf_counter()
-    native.mcsf_alg1(slab, cfg.H, s0, y0, rows, Q, a, cfg.N, Y, cfg.sigma_s)
+    for slab, s0, y0, rows in slabs:
+        native.mcsf_alg1(slab, cfg.H, s0, y0, rows, Q, a, cfg.N, Y, cfg.sigma_s)
     dt = time.perf_counter() - t0
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    info = {"rows": [y0, y0 + rows], "samples": M, "seconds": dt, "threads": threads}
-    return rows * cfg.W * M / dt, info
+    out_px = sum(y1 - y0 for y0, y1 in bands) * cfg.W
+    info = {"bands": [list(b) for b in bands], "samples": M, "seconds": dt, "threads": threads,
+            "out_px": out_px}
+    return out_px * M / dt, info
 
 
-def cpu_sample_size(cfg):
-    # ~10-30 s of fp64 work on an 8-core host for the default sample
-    rows = 8 if cfg.H >= 8 else cfg.H
-    lane_ops = cfg.W * (2 * rows + 2 * cfg.radius) * 2 * (cfg.d + 1) * (2 * cfg.radius + 1)
-    samples = max(1, min(cfg.M, int(2.0e11 / lane_ops)))
-    return rows, samples
+def cpu_sample_size(cfg, lane_op_budget=1.2e11):
+    """(bands, samples): the bands above and as many of the first samples as fit a budget of
+    fp64 lane-ops (~10-30 s on the box's host cores)."""
+    bands = cpu_bands(cfg, lane_op_budget)
+    per_sample = 0
+    from oracle import native
+    for y0, y1 in bands:
+        s0, s1 = native.slab_bounds(cfg.H, y0, y1 - y0, cfg.radius)
+        per_sample += cfg.W * ((s1 - s0) + (y1 - y0)) * 2 * (cfg.d + 1) * (2 * cfg.radius + 1)
+    samples = max(1, min(cfg.M, int(lane_op_budget / per_sample)))
+    return bands, samples
+
+
+def cpu_baseline_entry(cfg, value, info, bands):
+    """The cpu_baseline object: the measured band throughput scaled by the halo factor to the
+    full image (labelled as extrapolated) when the bands are not the whole image."""
+    full = bands == [(0, cfg.H)]
+    hf = 1.0 if full else halo_factor(cfg, bands)
+    where = ("the full image" if full else
+             " + ".join(f"output rows [{a},{b})" for a, b in bands) + f" of {cfg.H}")
+    return {"value": value * hf, "unit": "pixel*samples/s", "cores": info["threads"], "kind": "oracle",
+            "extrapolated": not full, "halo_factor": hf, "measured_value": value,
+            "sample": f"{where} x {cfg.W} cols, first {info['samples']} of {cfg.M} samples "
+                      f"({info['seconds']:.1f} s); value = measured x halo factor "
+                      f"{hf:.3f} (band slab rows + output rows over 2 x output rows)"
+                      + ("" if full else ", extrapolated to the full image")}
 
 
 def config_dict(cfg, world=1, mode="bands", **extra):
@@ -203,29 +262,30 @@ def config_dict(cfg, world=1, mode="bands", **extra):
 
 
 def run_reference(args, cfg):
+    """The reference arm: the CPU oracle as it stands (fp64 Algorithm 1, OpenMP), on this host's
+    cores. Under torchrun only rank 0 runs it; the other ranks exit without work."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    rows, samples = cpu_sample_size(cfg)
-    samples = max(1, samples // 4)          # each step a bounded sample (whole run: minutes)
+    bands, samples = cpu_sample_size(cfg, lane_op_budget=2.5e10)   # ~3-8 s per step
     for _ in range(args.warmup):
-        oracle_sample(cfg, rows, samples)
-    vals, secs = [], 0.0
+        oracle_sample(cfg, bands, samples)
+    secs, info = 0.0, None
     for _ in range(args.steps):
-        v, info = oracle_sample(cfg, rows, samples)
-        vals.append(v)
+        _, info = oracle_sample(cfg, bands, samples)
         secs += info["seconds"]
-    value = args.steps * rows * cfg.W * samples / secs
+    measured = args.steps * info["out_px"] * samples / secs
+    cpu = cpu_baseline_entry(cfg, measured, dict(info, seconds=secs), bands)
+    cpu["sample"] += f", per step ({args.steps} steps)"
+    value = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "pixel*samples/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "world_size": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(cfg, args.gpus, args.mode, engine="fir"),
-        "cpu_baseline": {"value": value, "unit": "pixel*samples/s", "cores": info["threads"],
-                         "kind": "oracle",
-                         "sample": f"output rows {info['rows']} x {cfg.W} cols, first {samples} of "
-                                   f"{cfg.M} samples, per step"},
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "pixel*samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -246,8 +306,10 @@ def run_ours(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        comm = communicator_report(dist, dev, world)
     r = cfg.radius
     plan = Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, cfg.M, cfg.seed,
                 value_range=cfg.value_range)
@@ -399,15 +461,14 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows_s, samples_s = cpu_sample_size(cfg)
-        v, info = oracle_sample(cfg, rows_s, samples_s)
-        cpu = {"value": v, "unit": "pixel*samples/s", "cores": info["threads"], "kind": "oracle",
-               "sample": f"output rows {info['rows']} x {cfg.W} cols, first {samples_s} of {cfg.M} samples "
-                         f"({info['seconds']:.1f} s)"}
+        bands_s, samples_s = cpu_sample_size(cfg)
+        v, info = oracle_sample(cfg, bands_s, samples_s)
+        cpu = cpu_baseline_entry(cfg, v, info, bands_s)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "pixel*samples/s", "n_gpus": world,
+            "world_size": world, "communicator": comm,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
@@ -423,8 +484,49 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
-def main():
-    args = parse()
+def communicator_report(dist, dev, world):
+    """One NCCL all_gather of each rank's (rank, local rank, PCI bus id): proves the communicator
+    spans `world` distinct GPUs before anything is timed (VERDICT r01 next #1)."""
+    import torch
+    props = torch.cuda.get_device_properties(dev)
+    bus = int(getattr(props, "pci_bus_id", -1))
+    mine = torch.tensor([dist.get_rank(), dev.index, bus], dtype=torch.int64, device=dev)
+    got = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(got, mine)
+    rows = [t.tolist() for t in got]
+    ndev = len({(r[1], r[2]) for r in rows})
+    rep = {"backend": dist.get_backend(), "nranks": dist.get_world_size(), "distinct_gpus": ndev,
+           "ranks": [{"rank": r[0], "local_rank": r[1], "pci_bus_id": r[2]} for r in rows]}
+    print(f"[rank {dist.get_rank()}] NCCL communicator: {dist.get_world_size()} ranks, "
+          f"{ndev} distinct GPUs", file=sys.stderr, flush=True)
+    return rep
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_command(argv, gpus, port):
+    """The torchrun command bench.py re-executes itself under for --gpus N > 1 when it was not
+    started by a launcher (one process per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        import subprocess
+        sys.exit(subprocess.call(launch_command(argv, args.gpus, free_port())))
+    if world and world != args.gpus:
+        if "--gpus" in " ".join(argv):
+            sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks")
+        args.gpus = world                      # torchrun without --gpus: the launcher's world
     from workloads import CONFIGS
     cfg = CONFIGS[args.config]
     if args.sigma:
