@@ -150,6 +150,11 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t plan, const float *f, int k0, in
  *   slots_per_rank  >= 1 and <= k1 - k0 (every group gets a sample)
  * Requires H % world == 0, the default FIR engine on the v6 kernel (d <= 3, 10 < r <= 48), no
  * colorspace (else BF_E_UNSUPPORTED). The caller maps peers' buffers (CUDA IPC).
+ * Reuse: a receive buffer may only be written again once its owner's bf_vec_normalize_slots of
+ * the previous call has completed. Frame-by-frame callers alternate two buffers (call n writes
+ * set n % 2) with a stream sync + barrier between the stores and the normalise of each call; a
+ * rank then cannot reach call n+2 before every owner finished normalising call n
+ * (paper_1605_02164_b200/shard.py P2PSlots).
  */
 bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t plan, const float *f, int k0, int k1,
                                       float *const *peer_slots, int world, int rank,
@@ -159,6 +164,9 @@ bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t plan, const float *f, int k0
  * bf_vec_normalize_slots -- Alg. 1 L231 on a receive buffer of bf_vec_filter_partial_p2p:
  * out_c = (sum_s P'_c,s) / (sum_s Z_s) + mu_c for rows [row0, row1) (the owner's band), summing
  * the nslots slots in order (deterministic). slots: device (nslots, D+1, row1-row0, W).
+ * The band must be the owner's band of the last bf_vec_filter_partial_p2p on this plan:
+ * row1 - row0 == H/world, row0 a multiple of H/world, nslots <= world * slots_per_rank, else
+ * BF_E_ARG; BF_E_STATE before any bf_vec_filter_partial_p2p.
  */
 bf_status_t bf_vec_normalize_slots(bf_vec_plan_t plan, const float *slots, int nslots, int row0,
                                    int row1, float *out_band, void *stream);

@@ -137,12 +137,12 @@ class Plan:
         n = (self.d + 1) * self.H * self.W
         if PZ is None:
             PZ = torch.empty(n, dtype=torch.float32, device=f.device)
+        # validated BEFORE the call: the kernel writes n floats through the raw pointer
+        if not isinstance(PZ, torch.Tensor) or PZ.numel() != n:
+            raise ValueError(f"PZ must hold (d+1)*H*W = {n} floats")
+        pz_ptr = _dev(PZ, tuple(PZ.shape), "PZ")
         check(self._lib.bf_vec_filter_partial(self._h, _dev(f, (self.d, self.H, self.W), "f"), int(k0), int(k1),
-                                              _dev(PZ, (PZ.numel(),), "PZ") if PZ.dim() == 1 else
-                                              _dev(PZ, tuple(PZ.shape), "PZ"), rpb, _stream_ptr(stream)),
-              "bf_vec_filter_partial")
-        if PZ.numel() != n:
-            raise ValueError("PZ must hold (d+1)*H*W floats")
+                                              pz_ptr, rpb, _stream_ptr(stream)), "bf_vec_filter_partial")
         return PZ
 
     def filter_partial_p2p(self, f, k0, k1, peer_slots, world, rank, slots_per_rank, stream=None):

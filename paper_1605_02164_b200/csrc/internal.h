@@ -205,6 +205,7 @@ struct bf_vec_plan_s {
     size_t drec_bytes = 0;
     int last_batch = 0;
     size_t free_mem = 0;       // free device memory at the first launch (0 = not queried yet)
+    int p2p_world = 0, p2p_slots = 0;   // layout of the last bf_vec_filter_partial_p2p (normalize_slots checks it)
     // CUDA-graph replay of bf_vec_filter (option "graph"): the launch sequence of a call is
     // captured on the second call with the same (f, out, stream, option generation) and replayed
     bool use_graph = true;

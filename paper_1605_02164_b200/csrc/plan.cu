@@ -176,6 +176,15 @@ size_t free_memory(bf_vec_plan_t p) {
     return p->free_mem > 1 ? p->free_mem : 0;
 }
 
+// An allocation failed: other users of the device (e.g. torch's caching allocator) took memory
+// since the cached query. Drop the cache and the failed error so the caller can re-plan its
+// scratch against what is free now and retry once.
+bool refresh_free_memory(bf_vec_plan_t p) {
+    cudaGetLastError();
+    p->free_mem = 0;
+    return free_memory(p) > 0;
+}
+
 // Choose (tile_rows, groups) for one fused launch by a simple cost model:
 // per CTA time ~ samples x (H-pass rows + V-pass rows + per-chunk overhead),
 // whole launch ~ waves x CTA time + the partial-sum traffic of G groups.
@@ -317,8 +326,14 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
     if (p2p) groups = p2p->slots;   // one receive slot per (rank, group) on every owner
     if (rb) groups = rb->groups;    // one realisation per group
     const KernelInfo &ki = p->kinfo;
-    const size_t img_pz = (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;   // partial floats per image
+    size_t img_pz = (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;   // partial floats per image
     bf_status_t st = ensure_pz(p, sizeof(float) * img_pz * nimg);
+    if (st == BF_E_CUDA && !p2p && !rb && refresh_free_memory(p)) {
+        // memory taken since the cached query: re-plan the groups against what is free now
+        choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups, nimg);
+        img_pz = (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;
+        st = ensure_pz(p, sizeof(float) * img_pz * nimg);
+    }
     if (st != BF_OK) return st;
     // reflect-padded, centred, interleaved copy of the rows this launch reads (pad.cu)
     const int R = ki.R;
@@ -520,25 +535,36 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     const size_t sum_h = (size_t)NQ * 2 * ntx * p->H, sum_v = (size_t)NQ * 2 * nty * p->W;
     const size_t uv_h = (size_t)NQ * 2 * p->H, uv_v = (size_t)NQ * 2 * p->W;
     const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v);
-    const size_t free_b = free_memory(p);
-    // batch: up to 256 samples within 40 % of the free memory, but no more than 16 samples or 4 GiB
-    // of summaries (whichever allows more) -- a larger batch only saves launches (5 per batch)
-    const double cap = std::max(16.0, 4.0 * 1024 * 1024 * 1024 / (double)per);
-    int nb = (int)std::max(1.0, std::min({256.0, 0.4 * (double)free_b / (double)per, cap}));
-    if (p->force_batch > 0) nb = p->force_batch;
-    nb = std::min(nb, ns);
-    // sample groups: enough CTAs for ~8 per SM where the tile count alone does not give them
-    const long long want = 8LL * sm_count();
-    const int g = (int)std::min<long long>(nb, std::max<long long>(1, (want + tiles - 1) / tiles));
-    if (p->drec_bytes < per * nb) {
-        cudaFree(p->drec);
-        p->drec = nullptr;
-        p->drec_bytes = 0;
-        BF_CUDA(cudaMalloc(&p->drec, per * nb));
-        p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
-        p->drec_bytes = per * nb;
+    int nb = 1, g = 1;
+    bf_status_t st = BF_OK;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const size_t free_b = free_memory(p);
+        // batch: up to 256 samples within 40 % of the free memory, but no more than 16 samples or
+        // 4 GiB of summaries (whichever allows more) -- a larger batch only saves launches (5 per batch)
+        const double cap = std::max(16.0, 4.0 * 1024 * 1024 * 1024 / (double)per);
+        nb = (int)std::max(1.0, std::min({256.0, 0.4 * (double)free_b / (double)per, cap}));
+        if (p->force_batch > 0) nb = p->force_batch;
+        nb = std::min(nb, ns);
+        // sample groups: enough CTAs for ~8 per SM where the tile count alone does not give them
+        const long long want = 8LL * sm_count();
+        g = (int)std::min<long long>(nb, std::max<long long>(1, (want + tiles - 1) / tiles));
+        st = BF_OK;
+        if (p->drec_bytes < per * nb) {
+            cudaFree(p->drec);
+            p->drec = nullptr;
+            p->drec_bytes = 0;
+            if (cudaMalloc(&p->drec, per * nb) != cudaSuccess) {
+                p->drec = nullptr;
+                st = BF_E_CUDA;
+            } else {
+                p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
+                p->drec_bytes = per * nb;
+            }
+        }
+        if (st == BF_OK) st = ensure_pz(p, sizeof(float) * (size_t)g * (p->d + 1) * px);
+        // memory taken since the cached query: re-plan the batch against what is free now
+        if (st != BF_E_CUDA || attempt == 1 || !refresh_free_memory(p)) break;
     }
-    bf_status_t st = ensure_pz(p, sizeof(float) * (size_t)g * (p->d + 1) * px);
     if (st != BF_OK) return st;
     RecTArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -599,13 +625,18 @@ bf_status_t run_recursive(bf_vec_plan_t p, const float *f, int k0, int k1, cudaS
     const size_t px = (size_t)p->H * p->W;
     // per sample in flight: y1 + y2 (2 x 2(d+1) planes) + one partial group ((d+1) planes)
     const double per = 4.0 * px * (4.0 * (p->d + 1) + (p->d + 1));
-    const size_t free_b = free_memory(p);
-    int nb = (int)std::max(1.0, std::min<double>(256.0, 0.4 * (double)free_b / per));
-    if (p->force_batch > 0) nb = p->force_batch;
-    nb = std::min(nb, ns);
-    bf_status_t st = ensure_rec_scratch(p, nb);
-    if (st != BF_OK) return st;
-    st = ensure_pz(p, sizeof(float) * (size_t)nb * (p->d + 1) * px);
+    int nb = 1;
+    bf_status_t st = BF_OK;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const size_t free_b = free_memory(p);
+        nb = (int)std::max(1.0, std::min<double>(256.0, 0.4 * (double)free_b / per));
+        if (p->force_batch > 0) nb = p->force_batch;
+        nb = std::min(nb, ns);
+        st = ensure_rec_scratch(p, nb);
+        if (st == BF_OK) st = ensure_pz(p, sizeof(float) * (size_t)nb * (p->d + 1) * px);
+        // memory taken since the cached query: re-plan the batch against what is free now
+        if (st != BF_E_CUDA || attempt == 1 || !refresh_free_memory(p)) break;
+    }
     if (st != BF_OK) return st;
     RecArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -940,6 +971,8 @@ bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t p, const float *f, int k0, i
     int groups = 1;
     bf_status_t st = run_fused(p, f, p->H, 0, 0, p->H, k0, k1, S(stream), &groups, &o);
     if (st != BF_OK) return st;
+    p->p2p_world = world;            // the receive-slot layout bf_vec_normalize_slots must match
+    p->p2p_slots = slots_per_rank;
     p->last_launches = 2;
     p->last = S(stream);
     return BF_OK;
@@ -949,7 +982,12 @@ bf_status_t bf_vec_normalize_slots(bf_vec_plan_t p, const float *slots, int nslo
                                    float *out_band, void *stream) {
     if (!valid_plan(p) || !slots || !out_band || nslots < 1) return BF_E_ARG;
     if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
-    if (p->device < 0 || !p->kinfo_ok) return BF_E_STATE;
+    if (p->device < 0 || !p->kinfo_ok || p->p2p_world < 1) return BF_E_STATE;
+    // the slots hold (D+1, H/world, W) planes of ONE owner's band: anything else would read past
+    // the receive buffer or misread its layout
+    const int band_rows = p->H / p->p2p_world;
+    if (row1 - row0 != band_rows || row0 % band_rows != 0 || nslots > p->p2p_world * p->p2p_slots)
+        return BF_E_ARG;
     cudaStream_t s = S(stream);
     fill_mu(p);
     BF_CUDA(launch_diag_reset(p->ddiag, s));

@@ -100,7 +100,14 @@ class P2PSlots:
     """This rank's receive buffer for `bf_vec_filter_partial_p2p` (world * slots_per_rank slots of
     (D+1, H/world, W) fp32) and the device pointers of every rank's buffer, mapped through CUDA IPC
     (cuda-python runtime bindings; the buffer is a plain cudaMalloc so its IPC handle covers it
-    exactly). world == 1 needs no IPC."""
+    exactly). world == 1 needs no IPC.
+
+    Reuse rule: there are TWO slot sets, used by alternate calls. After call n's
+    barrier a fast rank may start call n+1's kernel, storing into its peers' buffers while a slow
+    owner's normalise of call n is still queued; with one set that overwrote the partials being
+    normalised. Call n+1 writes the other set, and a rank can only reach call n+2 (which reuses
+    call n's set) after every owner passed call n+1's barrier -- by which point each owner has
+    synchronised its stream, so its normalise of call n has finished."""
 
     def __init__(self, plan, world: int, rank: int, slots_per_rank: int = 4, group=None):
         from cuda.bindings import runtime as rt
@@ -110,7 +117,9 @@ class P2PSlots:
         if plan.H % world:
             raise ValueError("P2P sample sharding needs H divisible by the world size")
         self.rows = plan.H // world
-        nbytes = world * slots_per_rank * (D + 1) * self.rows * plan.W * 4
+        self.set_bytes = world * slots_per_rank * (D + 1) * self.rows * plan.W * 4
+        self.calls = 0
+        nbytes = 2 * self.set_bytes
         err, ptr = rt.cudaMalloc(nbytes)
         if err != rt.cudaError_t.cudaSuccess:
             raise MemoryError(f"cudaMalloc({nbytes}) failed: {err}")
@@ -138,6 +147,12 @@ class P2PSlots:
             peers.append(int(pp))
         self.peers = peers
 
+    def next_set(self):
+        """(peer pointers, own pointer) of the slot set this call uses; alternates per call."""
+        off = (self.calls & 1) * self.set_bytes
+        self.calls += 1
+        return [p + off for p in self.peers], self.ptr + off
+
     def close(self):
         for pp in self._opened:
             self._rt.cudaIpcCloseMemHandle(pp)
@@ -154,13 +169,15 @@ def filter_samples_p2p(plan, f: torch.Tensor, slots: P2PSlots, group=None, out=N
     its own band from its slots. Returns (out_band, y0, y1)."""
     world, rank = slots.world, slots.rank
     k0, k1 = sample_range(plan.M, world, rank)
-    plan.filter_partial_p2p(f, k0, k1, slots.peers, world, rank, slots.slots_per_rank)
+    peers, mine = slots.next_set()            # alternate slot sets: see P2PSlots' reuse rule
+    plan.filter_partial_p2p(f, k0, k1, peers, world, rank, slots.slots_per_rank)
     if world > 1:
         torch.cuda.current_stream().synchronize()   # this rank's peer stores are complete ...
         dist.barrier(group)                          # ... and so are everyone else's
     y0 = rank * slots.rows
     y1 = y0 + slots.rows
-    return plan.normalize_slots(slots.ptr, world * slots.slots_per_rank, y0, y1, out=out, device=f.device), y0, y1
+    slots.last_ptr = mine
+    return plan.normalize_slots(mine, world * slots.slots_per_rank, y0, y1, out=out, device=f.device), y0, y1
 
 
 def gather_bands(out_band: torch.Tensor, H: int, group=None, band_fn=band) -> torch.Tensor:

@@ -38,6 +38,20 @@ def _rank(rank, world, port, outdir):
     spr = 4
     slots = shard.P2PSlots(p, world, rank, slots_per_rank=spr)
     try:
+        # frame-by-frame use: three calls, different images; rank 1 is made slow
+        # (a GPU sleep queued ahead of its normalise) so rank 0's next kernel stores into rank 1's
+        # buffer while rank 1 still has to normalise the previous call -- the alternating slot
+        # sets must keep the calls apart
+        for call, img in enumerate((f.flip(2).contiguous(), f.flip(1).contiguous())):
+            k0, k1 = shard.sample_range(p.M, world, rank)
+            peers, mine = slots.next_set()
+            p.filter_partial_p2p(img, k0, k1, peers, world, rank, slots.slots_per_rank)
+            torch.cuda.current_stream().synchronize()
+            dist.barrier()
+            if rank == 1:
+                torch.cuda._sleep(200_000_000)
+            ob = p.normalize_slots(mine, world * spr, rank * slots.rows, (rank + 1) * slots.rows, device=f.device)
+            np.save(os.path.join(outdir, f"frame{call}_band{rank}.npy"), ob.cpu().numpy())
         out, y0, y1 = shard.filter_samples_p2p(p, f, slots)
         np.save(os.path.join(outdir, f"band{rank}.npy"), out.cpu().numpy())
         np.save(os.path.join(outdir, f"rows{rank}.npy"), np.array([y0, y1]))
@@ -46,7 +60,7 @@ def _rank(rank, world, port, outdir):
         from cuda.bindings import runtime as rt
         D = p.info("kernel_D")
         raw = np.empty((world * spr, D + 1, slots.rows, cfg.W), dtype=np.float32)
-        err, = rt.cudaMemcpy(raw.ctypes.data, slots.ptr, raw.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+        err, = rt.cudaMemcpy(raw.ctypes.data, slots.last_ptr, raw.nbytes, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
         assert err == rt.cudaError_t.cudaSuccess
         np.save(os.path.join(outdir, f"zslots{rank}.npy"), raw[:, D].reshape(world, spr, slots.rows, cfg.W))
         dist.barrier()            # nobody unmaps a buffer a peer may still be reading
@@ -62,6 +76,10 @@ def test_two_rank_peer_exchange_matches_single_process():
     f = torch.from_numpy(make_image(cfg)).cuda()
     p = H.gpu_plan(cfg)
     ref = p.filter(f).cpu().numpy()
+    frames = [f.flip(2).contiguous(), f.flip(1).contiguous()]
+    frame_ref = [p.filter(g).cpu().numpy() for g in frames]
+    frame_ok = [p.filter_partial(g, 0, cfg.M).cpu().numpy().reshape(cfg.d + 1, cfg.H, cfg.W)[cfg.d] / cfg.M
+                >= H.Z_FLOOR for g in frames]
     Z = p.filter_partial(f, 0, cfg.M).cpu().numpy().reshape(cfg.d + 1, cfg.H, cfg.W)[cfg.d]
     half = p.filter_partial(f, 0, cfg.M // 2).cpu().numpy().reshape(cfg.d + 1, cfg.H, cfg.W)
     p.close()
@@ -70,6 +88,12 @@ def test_two_rank_peer_exchange_matches_single_process():
         bands = [np.load(os.path.join(d, f"band{r}.npy")) for r in range(2)]
         rows = [tuple(np.load(os.path.join(d, f"rows{r}.npy"))) for r in range(2)]
         zslots = [np.load(os.path.join(d, f"zslots{r}.npy")) for r in range(2)]
+        fr = [np.concatenate([np.load(os.path.join(d, f"frame{c}_band{r}.npy")) for r in range(2)], axis=1)
+              for c in range(2)]
+    for c in range(2):
+        e = np.abs(fr[c] - frame_ref[c])[:, frame_ok[c]].max()
+        print(f"frame {c}: two-rank P2P vs single process max |diff| = {e:.2e}")
+        assert e < 2e-3
     assert rows == [(0, cfg.H // 2), (cfg.H // 2, cfg.H)]
     got = np.concatenate(bands, axis=1)
     ok = Z / cfg.M >= H.Z_FLOOR

@@ -9,6 +9,7 @@ import torch
 
 from oracle import draws, filters, native
 from oracle import plan as oplan
+from paper_1605_02164_b200 import BfVecError
 from tests.gpu import helpers as H
 from workloads import CONFIGS, make_image, make_image_rows
 from workloads.configs import random_image, small_config
@@ -245,13 +246,37 @@ def test_p2p_sample_exchange_world1_matches_filter():
     Z = p.filter_partial(f, 0, cfg.M).cpu().numpy().reshape(cfg.d + 1, cfg.H, cfg.W)[cfg.d]
     slots = shard.P2PSlots(p, 1, 0, slots_per_rank=4)
     try:
+        with pytest.raises(BfVecError):         # before any p2p call: BF_E_STATE
+            p.normalize_slots(slots.ptr, 4, 0, cfg.H, device=f.device)
         out, y0, y1 = shard.filter_samples_p2p(p, f, slots)
         got = out.cpu().numpy()
+        # the band must be the owner's band of that call: a larger or shifted band
+        # or more slots than were written is refused instead of reading past the buffer
+        for bad in ((4, 0, cfg.H // 2), (4, 1, cfg.H), (5, 0, cfg.H)):
+            with pytest.raises(BfVecError):
+                p.normalize_slots(slots.last_ptr, bad[0], bad[1], bad[2], device=f.device)
     finally:
         slots.close()
     assert (y0, y1) == (0, cfg.H)
     ok = Z / cfg.M >= H.Z_FLOOR
     assert np.abs(got - ref)[:, ok].max() < 2e-3
+
+
+def test_filter_partial_rejects_short_pz_before_launch():
+    """an undersized PZ is refused before the kernel could write past it."""
+    cfg = CONFIGS[1]
+    f = torch.from_numpy(make_image(cfg)).cuda()
+    p = H.gpu_plan(cfg)
+    n = (cfg.d + 1) * cfg.H * cfg.W
+    guard = torch.full((n + 4096,), 7.0, device=f.device)
+    short = guard[: n - 1]
+    with pytest.raises(ValueError):
+        p.filter_partial(f, 0, cfg.M, PZ=short)
+    torch.cuda.synchronize()
+    assert bool((guard == 7.0).all())          # nothing was written
+    with pytest.raises(ValueError):
+        p.filter_partial(f, 0, cfg.M, PZ=guard[:n].view(cfg.d + 1, cfg.H, cfg.W).transpose(1, 2))
+    p.close()
 
 
 def test_graph_replay_bitwise_equals_eager():
