@@ -162,8 +162,11 @@ cudaError_t launch_srgb_to_lab(const float *in, float *out, long long npix, cuda
 cudaError_t launch_lab_to_srgb(const float *in, float *out, long long npix, cudaStream_t s);
 
 // Direct filter (direct.cu)
+// scratch UF: direct_scratch_bytes(d, H, W, r) (2d reflect-padded planes: U = A f, then f)
+size_t direct_scratch_bytes(int d, int H, int W, int r);
 cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const float *w,
-                          const float *A /* d x d: diag(alpha) Q^T scaled */, float *U,
+                          const float *A /* d x d: diag(alpha) Q^T scaled */,
+                          const float *mu /* d: centring (reading R12) */, float *UF,
                           float *out, cudaStream_t s);
 
 }  // namespace bfvec

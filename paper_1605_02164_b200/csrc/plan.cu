@@ -1036,7 +1036,7 @@ bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *str
     if (p->r > kMaxR) return BF_E_UNSUPPORTED;
     bf_status_t st = ensure_device(p);
     if (st != BF_OK) return st;
-    const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
+    const size_t bytes = direct_scratch_bytes(p->d, p->H, p->W, p->r);
     if (p->dU_bytes < bytes) {
         cudaFree(p->dU);
         p->dU = nullptr;
@@ -1054,7 +1054,8 @@ bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *str
         st = to_lab(p, f, p->H, &f, s);
         if (st != BF_OK) return st;
     }
-    BF_CUDA(launch_direct(f, p->d, p->H, p->W, p->r, p->taps, A, p->dU, out, s));
+    fill_mu(p);
+    BF_CUDA(launch_direct(f, p->d, p->H, p->W, p->r, p->taps, A, p->mu, p->dU, out, s));
     if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)p->H * p->W, s));
     p->last_launches = 2;
     p->last = s;
