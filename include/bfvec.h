@@ -246,6 +246,8 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *   "value_range" nominal data range R used for the alias warning (default 255)
  *   "tile_rows"   force the row-tile height of the fused kernel (0 = auto)
  *   "groups"      force the number of sample groups (0 = auto)
+ *   "direct_rows" bf_vec_direct: output rows per CTA, 4, 8 or 16 (0 = auto: 16 unless the
+ *                 image has fewer 16-row tiles than SMs)
  *   "variant"     fused-kernel variant: 0 auto (d <= 3: 4 where compiled, else 2, else 1;
  *                 5 <= d <= 8: 8),
  *                 1 shared-memory ring (v3), 2 tensor-memory ring (v4, d <= 3), 3 v4 with two

@@ -73,8 +73,7 @@ __global__ void direct_prep_kernel(const float *__restrict__ f, int d, int H, in
     }
 }
 
-constexpr int kDirTY = 16;                 // output rows per CTA (one per thread row)
-constexpr int kDirThreads = 256;           // 16 x 16 threads
+constexpr int kDirTYMax = 16;              // output rows per CTA (one per thread row): 4, 8 or 16
 constexpr int kDirLw = 2 * kMaxR + 1 + 16; // log2 spatial taps, padded to whole chunks
 
 struct DirectTArgs {
@@ -102,12 +101,12 @@ struct VecT<2> {
 };
 
 // Shared memory per CTA: ring of NS = TY + 1 rows x 2D planes x SW floats, then the taps.
-template <int D, int BX>
-__global__ void __launch_bounds__(kDirThreads) direct_tiled_kernel(const float *__restrict__ UF, int H, int W,
+template <int D, int BX, int TY>
+__global__ void __launch_bounds__(16 * TY) direct_tiled_kernel(const float *__restrict__ UF, int H, int W,
                                                                    int r, int Hp, int Wpp, int SW, int nch,
                                                                    const __grid_constant__ DirectTArgs da,
                                                                    float *__restrict__ out) {
-    constexpr int NP = 2 * D, TY = kDirTY, NS = TY + 1, TXW = 16 * BX;
+    constexpr int NP = 2 * D, NS = TY + 1, TXW = 16 * BX, kDirThreads = 16 * TY;
     extern __shared__ __align__(16) float dsm[];
     float *ring = dsm;
     float *s_lw = ring + (size_t)NS * NP * SW;
@@ -126,7 +125,7 @@ __global__ void __launch_bounds__(kDirThreads) direct_tiled_kernel(const float *
         }
         cp_async_commit();
     };
-    for (int i = tid; i < nch * BX; i += kDirThreads) s_lw[i] = da.lw[i];
+    for (int i = tid; i <= nch * BX; i += kDirThreads) s_lw[i] = i ? da.lw[i - 1] : -INFINITY;
     for (int k = 0; k < TY; ++k) load_row(k, k);
 
     // this thread's outputs: row y0 + ty, columns x0 + BX tx + b; centre values u_i
@@ -149,26 +148,48 @@ __global__ void __launch_bounds__(kDirThreads) direct_tiled_kernel(const float *
     // Two-level summation: each window row jy accumulates into (rden, rnum), added to the totals
     // once per row -- a single fp32 running sum over (2r+1)^2 terms loses ~(2r+1)^2 eps of the
     // sum (measured 1.3e-3 on config 3), two levels ~2 (2r+1) eps (7e-5, with the centring).
-    float rden[BX], rnum[D][BX];
-    // BX offsets jx = -r + BX ch + t (t < BX) for the thread's BX outputs: output b reads
-    // window pixel b + t of (lo | hi) = smem columns BX (tx + ch) .. BX (tx + ch + 2) - 1
+    //
+    // Packed pairs (FFMA2): output b (even) at offset index k and output b+1 at k-1 read the SAME
+    // source pixel b + k, so the pair's differences, quadratic forms and weighted sums are one
+    // FADD2 / FFMA2 each with the source broadcast; only the two ex2 are scalar. k runs over
+    // 0..nch*BX-1 >= 2r+1; lw[-1] and lw[k > 2r] are -inf (zero weight), so each output still
+    // sees exactly the offsets 0..2r.
+    constexpr int BH = BX / 2;
+    float2 rden[BH], rnum[D][BH], den2[BH], num2[D][BH], ui2[D][BH];
+#pragma unroll
+    for (int h = 0; h < BH; ++h) {
+        den2[h] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            num2[c][h] = make_float2(0.f, 0.f);
+            ui2[c][h] = make_float2(-ui[c][2 * h], -ui[c][2 * h + 1]);
+        }
+    }
+    // the chunk of offset indices k = BX ch + t (t < BX): pair h reads window pixel 2h + t of
+    // (lo | hi) = smem columns BX (tx + ch) .. BX (tx + ch + 2) - 1
     auto chunk = [&](const float (&lo)[NP][BX], const float (&hi)[NP][BX], float lwy, int ch) {
 #pragma unroll
         for (int t = 0; t < BX; ++t) {
-            const float lwt = lwy + s_lw[BX * ch + t];
+            // (lw[k] + lwy, lw[k-1] + lwy); s_lw is shifted by one so index k-1 = -1 exists
+            const float2 lwt = __fadd2_rn(make_float2(s_lw[BX * ch + t + 1], s_lw[BX * ch + t]),
+                                          make_float2(lwy, lwy));
 #pragma unroll
-            for (int b = 0; b < BX; ++b) {
-                const int s = b + t;
-                float q = lwt;
+            for (int h = 0; h < BH; ++h) {
+                const int s = 2 * h + t;
+                float2 q = lwt;
 #pragma unroll
                 for (int c = 0; c < D; ++c) {
-                    const float du = (s < BX ? lo[c][s] : hi[c][s - BX]) - ui[c][b];
-                    q = fmaf(-du, du, q);
+                    const float v = s < BX ? lo[c][s] : hi[c][s - BX];
+                    const float2 du = __fadd2_rn(make_float2(v, v), ui2[c][h]);
+                    q = __ffma2_rn(make_float2(-du.x, -du.y), du, q);
                 }
-                const float w = ex2_approx(q);
-                rden[b] += w;
+                const float2 w = make_float2(ex2_approx(q.x), ex2_approx(q.y));
+                rden[h] = __fadd2_rn(rden[h], w);
 #pragma unroll
-                for (int c = 0; c < D; ++c) rnum[c][b] = fmaf(w, s < BX ? lo[D + c][s] : hi[D + c][s - BX], rnum[c][b]);
+                for (int c = 0; c < D; ++c) {
+                    const float v = s < BX ? lo[D + c][s] : hi[D + c][s - BX];
+                    rnum[c][h] = __ffma2_rn(w, make_float2(v, v), rnum[c][h]);
+                }
             }
         }
     };
@@ -176,13 +197,13 @@ __global__ void __launch_bounds__(kDirThreads) direct_tiled_kernel(const float *
     int slot = ty;               // ring slot of padded row y0 + ty + q
     for (int q = 0; q <= 2 * r; ++q) {
         if (q < 2 * r) load_row(q + TY, (q + TY) % NS);   // the slot step q - 1 released
-        const float lwy = s_lw[q];
+        const float lwy = s_lw[q + 1];
         const float *srow = ring + (size_t)slot * NP * SW + BX * tx;
 #pragma unroll
-        for (int b = 0; b < BX; ++b) {
-            rden[b] = 0.f;
+        for (int h = 0; h < BH; ++h) {
+            rden[h] = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int c = 0; c < D; ++c) rnum[c][b] = 0.f;
+            for (int c = 0; c < D; ++c) rnum[c][h] = make_float2(0.f, 0.f);
         }
         float A[NP][BX], B[NP][BX];
 #pragma unroll
@@ -202,14 +223,24 @@ __global__ void __launch_bounds__(kDirThreads) direct_tiled_kernel(const float *
             chunk(A, B, lwy, ch);
         }
 #pragma unroll
-        for (int b = 0; b < BX; ++b) {
-            den[b] += rden[b];
+        for (int h = 0; h < BH; ++h) {
+            den2[h] = __fadd2_rn(den2[h], rden[h]);
 #pragma unroll
-            for (int c = 0; c < D; ++c) num[c][b] += rnum[c][b];
+            for (int c = 0; c < D; ++c) num2[c][h] = __fadd2_rn(num2[c][h], rnum[c][h]);
         }
         slot = slot + 1 == NS ? 0 : slot + 1;
         cp_async_wait_all();
         __syncthreads();
+    }
+#pragma unroll
+    for (int h = 0; h < BH; ++h) {
+        den[2 * h] = den2[h].x;
+        den[2 * h + 1] = den2[h].y;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            num[c][2 * h] = num2[c][h].x;
+            num[c][2 * h + 1] = num2[c][h].y;
+        }
     }
     if (y >= H) return;
     const long long npix = (long long)H * W;
@@ -225,24 +256,35 @@ __global__ void __launch_bounds__(kDirThreads) direct_tiled_kernel(const float *
 template <int D>
 constexpr int dir_bx() { return D <= 4 ? 4 : 2; }
 
-template <int D>
-cudaError_t launch_direct_d(const float *UF, int H, int W, int r, int Hp, int Wpp, int SW, int nch,
-                            const DirectTArgs &da, float *out, cudaStream_t s) {
+template <int D, int TY>
+cudaError_t launch_direct_dt(const float *UF, int H, int W, int r, int Hp, int Wpp, int SW, int nch,
+                             const DirectTArgs &da, float *out, cudaStream_t s) {
     constexpr int BX = dir_bx<D>();
-    constexpr int NP = 2 * D, NS = kDirTY + 1;
-    const size_t smem = sizeof(float) * ((size_t)NS * NP * SW + kDirLw);
+    constexpr int NP = 2 * D, NS = TY + 1;
+    const size_t smem = sizeof(float) * ((size_t)NS * NP * SW + kDirLw + 4);
     // the attribute is set once per device, so set it for the largest window (r = kMaxR)
-    constexpr int nch_max = (2 * kMaxR + 1 + BX - 1) / BX;
+    constexpr int nch_max = (2 * kMaxR + 2 + BX - 1) / BX;
     constexpr int SW_max = (16 * BX + BX * (nch_max + 2) + 3) / 4 * 4;
-    constexpr size_t smem_max = sizeof(float) * ((size_t)NS * NP * SW_max + kDirLw);
+    constexpr size_t smem_max = sizeof(float) * ((size_t)NS * NP * SW_max + kDirLw + 4);
     static_assert(smem_max <= 227 * 1024, "direct ring exceeds shared memory");
     if (smem > smem_max) return cudaErrorInvalidValue;
     static std::atomic<uint64_t> attr_done{0};
-    cudaError_t e = ensure_smem_attr(direct_tiled_kernel<D, BX>, smem_max, attr_done);
+    cudaError_t e = ensure_smem_attr(direct_tiled_kernel<D, BX, TY>, smem_max, attr_done);
     if (e != cudaSuccess) return e;
-    dim3 grid((W + 16 * BX - 1) / (16 * BX), (H + kDirTY - 1) / kDirTY);
-    direct_tiled_kernel<D, BX><<<grid, kDirThreads, smem, s>>>(UF, H, W, r, Hp, Wpp, SW, nch, da, out);
+    dim3 grid((W + 16 * BX - 1) / (16 * BX), (H + TY - 1) / TY);
+    direct_tiled_kernel<D, BX, TY><<<grid, 16 * TY, smem, s>>>(UF, H, W, r, Hp, Wpp, SW, nch, da, out);
     return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_direct_d(int ty, const float *UF, int H, int W, int r, int Hp, int Wpp, int SW, int nch,
+                            const DirectTArgs &da, float *out, cudaStream_t s) {
+    switch (ty) {
+        case 4: return launch_direct_dt<D, 4>(UF, H, W, r, Hp, Wpp, SW, nch, da, out, s);
+        case 8: return launch_direct_dt<D, 8>(UF, H, W, r, Hp, Wpp, SW, nch, da, out, s);
+        case 16: return launch_direct_dt<D, 16>(UF, H, W, r, Hp, Wpp, SW, nch, da, out, s);
+    }
+    return cudaErrorInvalidValue;
 }
 
 // geometry of the padded planes for (d, H, W, r): BX, chunks, smem row width, padded extents
@@ -253,10 +295,10 @@ DirectGeom direct_geom(int d, int H, int W, int r) {
     DirectGeom g;
     g.bx = d <= 4 ? 4 : 2;
     const int TXW = 16 * g.bx;
-    g.nch = (2 * r + 1 + g.bx - 1) / g.bx;
+    g.nch = (2 * r + 2 + g.bx - 1) / g.bx;   // offset indices k = 0..2r+1 (packed pairs: b at k, b+1 at k-1)
     g.SW = (TXW + g.bx * (g.nch + 2) + 3) / 4 * 4;   // the last chunk's window + the ping-pong overread
-    const int ntx = (W + TXW - 1) / TXW, nty = (H + kDirTY - 1) / kDirTY;
-    g.Hp = nty * kDirTY + 2 * r;
+    const int ntx = (W + TXW - 1) / TXW, nty = (H + kDirTYMax - 1) / kDirTYMax;
+    g.Hp = nty * kDirTYMax + 2 * r;   // whole 16-row tiles: covers every TY in {4, 8, 16}
     g.Wpp = ((ntx - 1) * TXW + g.SW + 3) / 4 * 4;
     return g;
 }
@@ -269,7 +311,7 @@ size_t direct_scratch_bytes(int d, int H, int W, int r) {
 }
 
 cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const float *w, const float *A,
-                          const float *mu, float *UF, float *out, cudaStream_t s) {
+                          const float *mu, float *UF, float *out, int rows_per_cta, cudaStream_t s) {
     if (r > kMaxR || d < 1 || d > kMaxD) return cudaErrorInvalidValue;
     const DirectGeom g = direct_geom(d, H, W, r);
     RotArgs ra{};
@@ -279,13 +321,14 @@ cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const floa
     direct_prep_kernel<<<(unsigned)((plane + 255) / 256), 256, 0, s>>>(f, d, H, W, r, g.Hp, g.Wpp, ra, UF);
     DirectTArgs da{};
     for (int c = 0; c < d; ++c) da.mu[c] = mu[c];
+    const int ty = rows_per_cta;   // 4, 8 or 16 (plan.cu picks it)
     for (int i = 0; i < kDirLw; ++i) {
         const int j = i - r;
         da.lw[i] = (j <= r && w[j < 0 ? -j : j] > 0.f) ? log2f(w[j < 0 ? -j : j]) : -INFINITY;
     }
     switch (d) {
 #define BFV_D(DD) \
-    case DD: return launch_direct_d<DD>(UF, H, W, r, g.Hp, g.Wpp, g.SW, g.nch, da, out, s);
+    case DD: return launch_direct_d<DD>(ty, UF, H, W, r, g.Hp, g.Wpp, g.SW, g.nch, da, out, s);
         BFV_D(1) BFV_D(2) BFV_D(3) BFV_D(4) BFV_D(5) BFV_D(6) BFV_D(7) BFV_D(8)
 #undef BFV_D
         default: return cudaErrorInvalidValue;

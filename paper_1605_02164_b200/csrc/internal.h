@@ -167,7 +167,7 @@ size_t direct_scratch_bytes(int d, int H, int W, int r);
 cudaError_t launch_direct(const float *f, int d, int H, int W, int r, const float *w,
                           const float *A /* d x d: diag(alpha) Q^T scaled */,
                           const float *mu /* d: centring (reading R12) */, float *UF,
-                          float *out, cudaStream_t s);
+                          float *out, int rows_per_cta /* 4, 8, 16 */, cudaStream_t s);
 
 }  // namespace bfvec
 
@@ -185,6 +185,7 @@ struct bf_vec_plan_s {
     double value_range = 255.0;
     int force_tile_rows = 0;
     int force_groups = 0;
+    int force_direct_rows = 0; // exact filter: output rows per CTA (0 auto, 4, 8, 16)
     int force_variant = 0;     // 0 auto, 1 v3 (smem ring), 2 v4 (TMEM ring)
     int spatial = 0;           // spatial taps: 0 Gaussian (Eq. (1)), 1 box, 2 hat (reading R15)
     int engine = 0;            // 0 truncated FIR (Eq. (1) window), 1 recursive Deriche (reading R16)

@@ -1055,7 +1055,15 @@ bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *str
         if (st != BF_OK) return st;
     }
     fill_mu(p);
-    BF_CUDA(launch_direct(f, p->d, p->H, p->W, p->r, p->taps, A, p->mu, p->dU, out, s));
+    // rows per CTA: 16 (measured fastest from 512^2 up, profiles/r02_direct_rows_sweep.txt) unless
+    // the image has fewer 16-row tiles than SMs; option "direct_rows" forces it
+    int ty = p->force_direct_rows;
+    if (ty <= 0) {
+        const long long ntx = (p->W + 16 * (p->d <= 4 ? 4 : 2) - 1) / (16 * (p->d <= 4 ? 4 : 2));
+        ty = 16;
+        while (ty > 4 && ntx * ((p->H + ty - 1) / ty) < sm_count()) ty /= 2;
+    }
+    BF_CUDA(launch_direct(f, p->d, p->H, p->W, p->r, p->taps, A, p->mu, p->dU, out, ty, s));
     if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)p->H * p->W, s));
     p->last_launches = 2;
     p->last = s;
@@ -1230,6 +1238,11 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         return BF_OK;
     }
     if (!std::strcmp(name, "tile_rows")) { if (v < 0) return BF_E_ARG; p->force_tile_rows = (int)v; return BF_OK; }
+    if (!std::strcmp(name, "direct_rows")) {
+        if (v != 0.0 && v != 4.0 && v != 8.0 && v != 16.0) return BF_E_ARG;
+        p->force_direct_rows = (int)v;
+        return BF_OK;
+    }
     if (!std::strcmp(name, "groups")) { if (v < 0) return BF_E_ARG; p->force_groups = (int)v; return BF_OK; }
     if (!std::strcmp(name, "variant")) {
         if (v < 0 || v > 8) return BF_E_ARG;

@@ -32,8 +32,9 @@ def bound_s(pairs, d, mhz=MHZ):
     return max(fp32, mufu), ("fp32" if fp32 >= mufu else "mufu")
 
 
-def time_direct(cfg, f, reps):
+def time_direct(cfg, f, reps, rows=0):
     p = Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, cfg.M, cfg.seed, value_range=cfg.value_range)
+    p.set_option("direct_rows", rows)
     out = torch.empty_like(f)
     s = torch.cuda.current_stream()
     for _ in range(3):
@@ -57,6 +58,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--json", default="")
     ap.add_argument("--only", default="", help="run only cases whose name contains this")
+    ap.add_argument("--rows", type=int, default=0, help="option direct_rows (0 auto, 4, 8, 16)")
     args = ap.parse_args()
     rows = []
     c2 = CONFIGS[2]
@@ -72,11 +74,11 @@ def main():
             continue
         if f is None:
             f = torch.from_numpy(make_image(cfg)).cuda()
-        ms = time_direct(cfg, f, args.reps)
+        ms = time_direct(cfg, f, args.reps, args.rows)
         r = cfg.radius
         pairs = cfg.H * cfg.W * (2 * r + 1) ** 2
         b, which = bound_s(pairs, cfg.d)
-        row = {"case": name, "H": cfg.H, "W": cfg.W, "d": cfg.d, "sigma_s": cfg.sigma_s, "r": r, "ms": ms,
+        row = {"case": name, "direct_rows": args.rows, "H": cfg.H, "W": cfg.W, "d": cfg.d, "sigma_s": cfg.sigma_s, "r": r, "ms": ms,
                "pairs_per_s": pairs / (ms / 1e3), "bound_ms": b * 1e3, "bound": which,
                "frac_of_roofline": b * 1e3 / ms}
         rows.append(row)
