@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbfvec.so")
+LIB_PATH = os.environ.get("BFVEC_LIB") or os.path.join(_HERE, "libbfvec.so")   # BFVEC_LIB: A/B builds
 
 # names and signatures of every symbol declared in include/bfvec.h
 _P, _I, _D, _U64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_uint64

@@ -14,12 +14,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libbfvec.so")
+# A/B experiments: BFVEC_BUILD_TAG=x builds build/obj_x -> libbfvec_x.so with the extra nvcc flags
+# in BFVEC_NVCC_EXTRA (e.g. -DBFVEC_MBAR_SPIN); load it with BFVEC_LIB=<path> (_lib.py)
+TAG = os.environ.get("BFVEC_BUILD_TAG", "")
+OBJ = os.path.join(ROOT, "build", "obj" + (f"_{TAG}" if TAG else ""))
+LIB = os.path.join(HERE, f"libbfvec{'_' + TAG if TAG else ''}.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
+         *os.environ.get("BFVEC_NVCC_EXTRA", "").split()]
 
 
 def _sources():
@@ -49,7 +53,7 @@ def _compile(src, force):
     cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = res.stdout + res.stderr
-    with open(os.path.join(ROOT, "build", f"ptxas_{src}.log"), "w") as fh:
+    with open(os.path.join(ROOT, "build", f"ptxas_{src}{'_' + TAG if TAG else ''}.log"), "w") as fh:
         fh.write(log)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{log[-6000:]}")

@@ -2,6 +2,7 @@
 // (L210-214), scheduling of the fused kernel, and the
 // orchestration of the device kernels on the caller's stream.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -18,6 +19,17 @@ using namespace bfvec;
 namespace {
 
 inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// NVTX range over one C-ABI call (plan, sample, filter, partial, normalise, ...), so an nsys / ncu
+// timeline of a multi-GPU run shows each rank's phases by name (`ncu --nvtx --nvtx-include
+// "bfvec:filter/"` selects the kernels of one phase). Header-only NVTX3: a no-op unless a tool
+// is attached.
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx &) = delete;
+    Nvtx &operator=(const Nvtx &) = delete;
+};
 
 // ---------------------------------------------------------------------------
 // Eq. (4): C = Q diag(1/alpha^2) Q^T by cyclic Jacobi rotations
@@ -713,6 +725,7 @@ const char *bf_vec_status_string(bf_status_t st) {
 
 bf_status_t bf_vec_plan(int H, int W, int d, double sigma_s, const double *C, int N, int M,
                         uint64_t seed, bf_vec_plan_t *out) {
+    Nvtx nvtx_("bfvec:plan");
     if (!out || !C) return BF_E_ARG;
     *out = nullptr;
     if (H < 1 || W < 1 || d < 1 || d > kMaxD || M < 1) return BF_E_ARG;
@@ -758,6 +771,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
 }
 
 bf_status_t bf_vec_sample_freqs(bf_vec_plan_t p, void *stream) {
+    Nvtx nvtx_("bfvec:sample");
     if (!valid_plan(p)) return BF_E_ARG;
     bf_status_t st = ensure_device(p);
     if (st != BF_OK) return st;
@@ -878,6 +892,7 @@ bf_status_t filter_graph(bf_vec_plan_t p, const float *f, float *out, cudaStream
 }
 
 bf_status_t bf_vec_filter(bf_vec_plan_t p, const float *f, float *out, void *stream) {
+    Nvtx nvtx_("bfvec:filter");
     if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
     if (p->device < 0) return BF_E_STATE;
     cudaStream_t s = S(stream);
@@ -892,6 +907,7 @@ bf_status_t bf_vec_filter(bf_vec_plan_t p, const float *f, float *out, void *str
 }
 
 bf_status_t bf_vec_filter_batch(bf_vec_plan_t p, const float *f, float *out, int nimg, void *stream) {
+    Nvtx nvtx_("bfvec:filter_batch");
     if (!valid_plan(p) || !f || !out || f == out || nimg < 1) return BF_E_ARG;
     if (p->device < 0 || !p->sampled) return BF_E_STATE;
     if (p->engine != 0 || p->lab) return BF_E_UNSUPPORTED;
@@ -912,6 +928,7 @@ bf_status_t bf_vec_filter_batch(bf_vec_plan_t p, const float *f, float *out, int
 }
 
 bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {
+    Nvtx nvtx_("bfvec:filter_host");
     if (!valid_plan(p) || !f_host || !out_host) return BF_E_ARG;
     if (p->device < 0) return BF_E_STATE;
     const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
@@ -934,6 +951,7 @@ bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_
 
 bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k1, float *PZ,
                                   int rows_per_band, void *stream) {
+    Nvtx nvtx_("bfvec:filter_partial");
     if (!valid_plan(p) || !f || !PZ) return BF_E_ARG;
     if (k0 < 0 || k1 > p->M || k0 > k1 || rows_per_band < 1 || rows_per_band > p->H) return BF_E_ARG;
     if (p->device < 0 || !p->sampled) return BF_E_STATE;
@@ -959,6 +977,7 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k
 
 bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t p, const float *f, int k0, int k1, float *const *peer_slots,
                                       int world, int rank, int slots_per_rank, void *stream) {
+    Nvtx nvtx_("bfvec:filter_partial_p2p");
     if (!valid_plan(p) || !f || !peer_slots) return BF_E_ARG;
     if (world < 1 || world > 8 || rank < 0 || rank >= world || slots_per_rank < 1) return BF_E_ARG;
     if (k0 < 0 || k1 > p->M || k1 - k0 < slots_per_rank) return BF_E_ARG;   // every group non-empty
@@ -980,6 +999,7 @@ bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t p, const float *f, int k0, i
 
 bf_status_t bf_vec_normalize_slots(bf_vec_plan_t p, const float *slots, int nslots, int row0, int row1,
                                    float *out_band, void *stream) {
+    Nvtx nvtx_("bfvec:normalize_slots");
     if (!valid_plan(p) || !slots || !out_band || nslots < 1) return BF_E_ARG;
     if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
     if (p->device < 0 || !p->kinfo_ok || p->p2p_world < 1) return BF_E_STATE;
@@ -1000,6 +1020,7 @@ bf_status_t bf_vec_normalize_slots(bf_vec_plan_t p, const float *slots, int nslo
 
 bf_status_t bf_vec_normalize(bf_vec_plan_t p, const float *PZ_band, int row0, int row1, float *out_band,
                              void *stream) {
+    Nvtx nvtx_("bfvec:normalize");
     if (!valid_plan(p) || !PZ_band || !out_band) return BF_E_ARG;
     if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
     bf_status_t st = ensure_device(p);
@@ -1015,6 +1036,7 @@ bf_status_t bf_vec_normalize(bf_vec_plan_t p, const float *PZ_band, int row0, in
 
 bf_status_t bf_vec_filter_rows(bf_vec_plan_t p, const float *slab, int slab_row0, int slab_rows, int row0,
                                int row1, float *out_band, void *stream) {
+    Nvtx nvtx_("bfvec:filter_rows");
     if (!valid_plan(p) || !slab || !out_band) return BF_E_ARG;
     if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
     if (slab_row0 < 0 || slab_rows < 1 || slab_row0 + slab_rows > p->H) return BF_E_ARG;
@@ -1032,6 +1054,7 @@ bf_status_t bf_vec_filter_rows(bf_vec_plan_t p, const float *slab, int slab_row0
 }
 
 bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *stream) {
+    Nvtx nvtx_("bfvec:direct");
     if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
     if (p->r > kMaxR) return BF_E_UNSUPPORTED;
     bf_status_t st = ensure_device(p);
@@ -1072,6 +1095,7 @@ bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *str
 
 bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, int n_seeds, const uint64_t *seeds,
                              int n_t, const int *t_list, double *mse, void *stream) {
+    Nvtx nvtx_("bfvec:mse_sweep");
     if (!valid_plan(p) || !f || !ref || !seeds || !t_list || !mse || n_seeds < 1 || n_t < 1) return BF_E_ARG;
     for (int j = 0; j < n_t; ++j)
         if (t_list[j] < 1 || t_list[j] > p->M || (j > 0 && t_list[j] <= t_list[j - 1])) return BF_E_ARG;

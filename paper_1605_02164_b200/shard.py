@@ -22,8 +22,24 @@ the orchestration on CPU with gloo and a stand-in backend).
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 import torch.distributed as dist
+
+
+@contextlib.contextmanager
+def nvtx(name: str):
+    """NVTX range on the host timeline (the C ABI marks its own calls "bfvec:<call>"): the
+    exchange step of a multi-GPU run shows up by name next to them. No-op without CUDA."""
+    if torch.cuda.is_available():
+        torch.cuda.nvtx.range_push(name)
+        try:
+            yield
+        finally:
+            torch.cuda.nvtx.range_pop()
+    else:
+        yield
 
 
 def band(H: int, world: int, rank: int) -> tuple:
@@ -88,7 +104,8 @@ def filter_samples(plan, f: torch.Tensor, group=None, partial_fn=None, normalize
         normalize_fn = lambda PZb, a, b: plan.normalize(PZb, a, b, out=out)  # noqa: E731
     PZ = partial_fn(f, k0, k1, rpb).reshape(-1)
     PZ_band = torch.empty(counts[rank], dtype=PZ.dtype, device=PZ.device)
-    dist.reduce_scatter(PZ_band, list(torch.split(PZ, counts)), op=dist.ReduceOp.SUM, group=group)
+    with nvtx("bfvec:reduce_scatter"):
+        dist.reduce_scatter(PZ_band, list(torch.split(PZ, counts)), op=dist.ReduceOp.SUM, group=group)
     y0 = min(H, rank * rpb)
     y1 = min(H, y0 + rpb)
     if y1 <= y0:
@@ -172,8 +189,9 @@ def filter_samples_p2p(plan, f: torch.Tensor, slots: P2PSlots, group=None, out=N
     peers, mine = slots.next_set()            # alternate slot sets: see P2PSlots' reuse rule
     plan.filter_partial_p2p(f, k0, k1, peers, world, rank, slots.slots_per_rank)
     if world > 1:
-        torch.cuda.current_stream().synchronize()   # this rank's peer stores are complete ...
-        dist.barrier(group)                          # ... and so are everyone else's
+        with nvtx("bfvec:p2p_barrier"):
+            torch.cuda.current_stream().synchronize()   # this rank's peer stores are complete ...
+            dist.barrier(group)                          # ... and so are everyone else's
     y0 = rank * slots.rows
     y1 = y0 + slots.rows
     slots.last_ptr = mine
