@@ -124,6 +124,26 @@ bf_status_t bf_vec_filter_host(bf_vec_plan_t plan, const float *f_host, float *o
                                void *stream);
 
 /*
+ * bf_vec_filter_host_async -- bf_vec_filter_host for a stream of frames: enqueues the H2D copy of
+ * f_host (on a plan-owned copy stream), the filter (on `stream`, after the copy) and the D2H copy
+ * into out_host (on a second copy stream, after the filter) and returns without waiting, so frame
+ * i+1's input copy and frame i-1's output copy overlap frame i's kernels. Results are bitwise those
+ * of bf_vec_filter_host. The plan alternates two device slots per direction; reusing a slot waits
+ * (on the device) for the frame that used it two calls earlier.
+ *   f_host, out_host  host (d, H, W) fp32; pinned (cudaHostAlloc / torch pin_memory) for the copies
+ *                     to be asynchronous. The caller must keep f_host unchanged and out_host alive
+ *                     until bf_vec_host_sync returns (or alternate host buffers per frame).
+ * Errors: BF_E_STATE before bf_vec_sample_freqs; BF_E_CUDA.
+ */
+bf_status_t bf_vec_filter_host_async(bf_vec_plan_t plan, const float *f_host, float *out_host, void *stream);
+
+/*
+ * bf_vec_host_sync -- wait until every bf_vec_filter_host_async frame enqueued on this plan has been
+ * copied back to its out_host buffer.
+ */
+bf_status_t bf_vec_host_sync(bf_vec_plan_t plan);
+
+/*
  * bf_vec_filter_partial -- raw sums over samples k in [k0, k1) only
  * (0 <= k0 <= k1 <= M), for sample sharding (one NCCL sum afterwards).
  *   PZ         device float32, (d+1) planes per row band: for band b covering

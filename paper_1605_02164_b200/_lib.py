@@ -19,6 +19,8 @@ SIGNATURES = {
     "bf_vec_get_draws": ([_P, _P, _P, _P, _P], _I),
     "bf_vec_filter": ([_P, _P, _P, _P], _I),
     "bf_vec_filter_host": ([_P, _P, _P, _P], _I),
+    "bf_vec_filter_host_async": ([_P, _P, _P, _P], _I),
+    "bf_vec_host_sync": ([_P], _I),
     "bf_vec_filter_batch": ([_P, _P, _P, _I, _P], _I),
     "bf_vec_filter_partial": ([_P, _P, _I, _I, _P, _I, _P], _I),
     "bf_vec_normalize": ([_P, _P, _I, _I, _P, _P], _I),

@@ -132,6 +132,22 @@ class Plan:
             _stream_ptr(stream)), "bf_vec_filter_host")
         return out_host
 
+    def filter_host_async(self, f_host, out_host, stream=None):
+        """bf_vec_filter_host_async: enqueue one frame (pinned host tensors in and out) and return;
+        the result is in out_host after host_sync(). Keep f_host / out_host alive until then."""
+        shp = (self.d, self.H, self.W)
+        for t, n in ((f_host, "f_host"), (out_host, "out_host")):
+            if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous() or tuple(t.shape) != shp:
+                raise ValueError(f"{n} must be a contiguous float32 host tensor of shape {shp}")
+        self.last_status = check(self._lib.bf_vec_filter_host_async(
+            self._h, ctypes.c_void_p(f_host.data_ptr()), ctypes.c_void_p(out_host.data_ptr()),
+            _stream_ptr(stream)), "bf_vec_filter_host_async")
+        return out_host
+
+    def host_sync(self):
+        """bf_vec_host_sync: every enqueued filter_host_async frame is in its out_host."""
+        check(self._lib.bf_vec_host_sync(self._h), "bf_vec_host_sync")
+
     def filter_partial(self, f, k0, k1, PZ=None, rows_per_band=None, stream=None):
         rpb = self.H if rows_per_band is None else int(rows_per_band)
         n = (self.d + 1) * self.H * self.W

@@ -237,6 +237,12 @@ struct bf_vec_plan_s {
     size_t dU_bytes = 0;
     float *dhost_in = nullptr, *dhost_out = nullptr;
     size_t dhost_bytes = 0;
+    // bf_vec_filter_host_async: two device slots per direction, copy streams and their events
+    float *dasync_in[2] = {nullptr, nullptr}, *dasync_out[2] = {nullptr, nullptr};
+    size_t dasync_bytes = 0;
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    long long async_calls = 0;
     float mu[8];
     cudaStream_t last = nullptr;
     // last schedule

@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include <atomic>
 #include <utility>
 
@@ -40,10 +42,40 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 // in a loop: the spinning modulation / consumer warps no longer take issue slots from the FIR warps
 // (BRA was 13-18 % of the fused kernels' PC samples). -DBFVEC_MBAR_SPIN restores the
 // plain probe loop for A/B measurements.
+//
+// Checked build (-DBFVEC_CHECKED, tools/checked_build.sh; the stand-in for compute-sanitizer, which
+// this pool does not run): every wait has a watchdog -- a phase that does not complete within
+// ~2^24 probes of <= 1 us (seconds) is a protocol deadlock: the kernel prints the barrier and
+// traps instead of hanging the GPU. BF_CHECK(cond) traps with the failed condition.
+#ifdef BFVEC_CHECKED
+constexpr uint32_t kMbarSuspendNs = 1000;
+#define BF_CHECK(cond)                                                                                     \
+    do {                                                                                                   \
+        if (!(cond)) {                                                                                     \
+            printf("BF_CHECK failed: %s (%s:%d) block (%d,%d,%d) thread %d\n", #cond, __FILE__, __LINE__,    \
+                   blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);                                       \
+            __trap();                                                                                      \
+        }                                                                                                  \
+    } while (0)
+#else
 constexpr uint32_t kMbarSuspendNs = 0x989680;   // 10 ms upper bound; the phase completion wakes the warp
+#define BF_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done;
+#ifdef BFVEC_CHECKED
+    uint32_t probes = 0;
+#endif
     do {
+#ifdef BFVEC_CHECKED
+        if (++probes == (1u << 24)) {
+            printf("mbar_wait watchdog: barrier %p parity %u never completed (block (%d,%d,%d) thread %d)\n",
+                   (void *)bar, parity, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);
+            __trap();
+        }
+#endif
 #ifdef BFVEC_MBAR_SPIN
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"

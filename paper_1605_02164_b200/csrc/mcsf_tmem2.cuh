@@ -57,7 +57,16 @@ struct CfgT2 {
     static constexpr int SZ_TP = (NA / 32) * TX * 9 * 8;      // per producer warp: 32 columns x 9 float2
     static constexpr int OFF_TP = round_up(OFF_RING + SP * SZ_RING, 128);
     static constexpr int OFF_BAR = round_up(OFF_TP + SZ_TP, 128);
+#ifdef BFVEC_CHECKED
+    // checked build: row tags of every ring slot (TMEM ring per (sample, pair), (c, s) ring per
+    // sample) and the sub-step id held by each G buffer -- the consumers verify that every slot
+    // they read still holds the row they expect, before and after reading it
+    static constexpr int OFF_TAG = OFF_BAR + 128;
+    static constexpr int NTAG = SP * 4 * HROWS + SP * RING + 2;
+    static constexpr size_t SMEM = OFF_TAG + 4 * NTAG;
+#else
     static constexpr size_t SMEM = OFF_BAR + 9 * 8 + 8;    // tma, full[2], empty[2], gfull[2], gempty[2]
+#endif
     static constexpr uint32_t TMA_BYTES = SZ_F;
     static_assert(D >= 1 && D <= 3, "one TMEM lane quarter per pair");
     static_assert(CW_ == 1 || CW_ == 2, "one or two consumer warps per pair");
@@ -166,7 +175,9 @@ __device__ __forceinline__ void box_hpass(const FusedArgs &a, const float2 *row,
 // modulation of one SH-row sub-step for the pass's samples (np of them) into G[buf][s]
 template <class C, int NTH>
 __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0, float2 *gb1, float2 *cs0,
-                                          float2 *cs1, const float (&tk)[2][C::D], int g0, int np) {
+                                          float2 *cs1, const float (&tk)[2][C::D], int g0, int np,
+                                          int *cstag = nullptr) {
+    (void)cstag;
     constexpr int PER = (C::SH * C::WIN + NTH - 1) / NTH;
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
@@ -194,6 +205,9 @@ __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0
             for (int p = 1; p < C::NP; ++p)
                 dst[p * C::SH * C::MS] = __fmul2_rn(make_float2(cn, sn), make_float2(fv[p - 1], fv[p - 1]));
             if (inner) (s == 0 ? cs0 : cs1)[rs] = make_float2(cn, sn);
+#ifdef BFVEC_CHECKED
+            if (j == C::R) cstag[s * C::RING + (g0 + row) % C::RING] = g0 + row;
+#endif
         }
     }
 }
@@ -211,6 +225,14 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
     uint64_t *gfull = tma_bar + 5;    // modulators -> H-pass producers, per G buffer
     uint64_t *gempty = tma_bar + 7;   // H-pass producers -> modulators
     uint32_t *taddr_s = reinterpret_cast<uint32_t *>(tma_bar + 9);
+#ifdef BFVEC_CHECKED
+    int *ttag = reinterpret_cast<int *>(smem + C::OFF_TAG);          // [SP][4][HROWS]
+    int *cstag = ttag + C::SP * 4 * C::HROWS;                         // [SP][RING]
+    int *gtag = cstag + C::SP * C::RING;                              // [2]
+    for (int i = threadIdx.x; i < C::NTAG; i += C::NT) ttag[i] = -1;
+#else
+    int *cstag = nullptr;
+#endif
     constexpr int GSZ = C::NP * C::SH * C::MS;     // float2 per (buffer, slot)
     constexpr int CSZ = C::RING * C::TX;           // float2 per slot's (c, s) ring
 
@@ -292,7 +314,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                         if constexpr (C::MW == 0) {
                             mbar_wait(tma_bar, tparity);
                             tparity ^= 1u;
-                            modulate2<C, C::NA>(ta, fbuf, gb0, gb1, csbase, csbase + CSZ, tk, gsub, np);
+                            modulate2<C, C::NA>(ta, fbuf, gb0, gb1, csbase, csbase + CSZ, tk, gsub, np, cstag);
                             named_sync<C::NA>(1);   // G-pairs complete; fbuf free; previous H-pass done
                             if (ta == 0) {
                                 int nu = -1;
@@ -303,6 +325,9 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                             }
                         } else {
                             mbar_wait(&gfull[buf], (it >> 1) & 1);   // the modulators filled G[buf]
+#ifdef BFVEC_CHECKED
+                            BF_CHECK(gtag[buf] == it);
+#endif
                         }
                         if (p < C::NP && sw < np) {
                             // horizontal FIR: 8 outputs (row r8, columns 8cg .. 8cg+7) of sample sw
@@ -320,6 +345,9 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                                     fir_input<C, 8, 2 * jj + 1>(a, acc, early, make_float2(v2.z, v2.w));
                                 });
                             }
+#ifdef BFVEC_CHECKED
+                            if constexpr (C::MW > 0) BF_CHECK(gtag[buf] == it);   // not refilled while read
+#endif
                             if constexpr (C::MW > 0) mbar_arrive(&gempty[buf]);   // G[buf] read
                             // transpose through this warp's shared-memory tile: lane (r8, cg) holds
                             // row r8 of columns 8cg..8cg+7; lane x needs rows 0..7 of column x.
@@ -332,7 +360,11 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                             for (int o = 0; o < 8; ++o) acc[o] = tt[lane * 9 + o];
                             __syncwarp();
                             const int slot = gsub % C::HROWS;   // 8 consecutive slots, no wrap
+                            BF_CHECK(slot + 8 <= C::HROWS);
                             tmem_st16(tq + 2 * slot, acc);
+#ifdef BFVEC_CHECKED
+                            if (lane < 8) ttag[(sw * 4 + p) * C::HROWS + slot + lane] = gsub + lane;
+#endif
                         } else if constexpr (C::MW > 0) {
                             mbar_arrive(&gempty[buf]);
                         }
@@ -373,8 +405,11 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                             mbar_wait(tma_bar, tparity);
                             tparity ^= 1u;
                             modulate2<C, C::NM>(tm, fbuf, gbase + (2 * buf) * GSZ, gbase + (2 * buf + 1) * GSZ, csbase,
-                                                csbase + CSZ, tk, gsub, np);
+                                                csbase + CSZ, tk, gsub, np, cstag);
                             named_sync<C::NM>(2);   // fbuf consumed by every modulator
+#ifdef BFVEC_CHECKED
+                            if (tm == 0) gtag[buf] = it;
+#endif
                             if (tm == 0) {
                                 int nu = -1;
                                 if (s0 + C::SH < n_new) nu = u_begin + s0 + C::SH;
@@ -444,6 +479,21 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                             });
                             if constexpr (bj + 1 < JB1) tmem_wait_rows<LR>(v[(bj + 1) & 1]);
                         });
+#ifdef BFVEC_CHECKED
+                        if (active && lane == 0) {
+                            // every TMEM ring row of this window (loaded above) must still be the
+                            // row the window expects, after the loads completed
+                            for (int j = 0; j < JB1 * LR; ++j) {
+                                const int sl = (b0 + j) % C::HROWS;
+                                const int want = gs + ci * C::KB + H0 + j;
+                                if (j < C::OR + 2 * C::R) BF_CHECK(ttag[(s * 4 + p) * C::HROWS + sl] == want);
+                            }
+                            for (int o = 0; o < OR; ++o) {
+                                const int row = gs + ci * C::KB + H0 + C::R + o;
+                                BF_CHECK(cstag[s * C::RING + row % C::RING] == row);
+                            }
+                        }
+#endif
                         const float2 *csr = csbase + s * CSZ;
                         int slot = (gs + ci * C::KB + H0 + C::R) % C::RING;
 #pragma unroll

@@ -156,7 +156,11 @@ cudaError_t launch_normalize_groups(const float *pz, int groups, int D, int d, i
     const long long npix = (long long)rows * W;
     const int threads = 256;
     auto dg = reinterpret_cast<unsigned long long *>(diag);
-    if (W % 4 == 0) {
+    // float4 path only when every row starts 16-byte aligned in both buffers (out is the caller's
+    // pointer: a view may start anywhere; the scalar path serves the rest)
+    const bool vec_ok = W % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                        (reinterpret_cast<uintptr_t>(pz) & 15) == 0;
+    if (vec_ok) {
         const long long n = npix / 4;
         normalize_groups_kernel<4><<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
             pz, groups, D, d, npix, nullptr, mu[0], mu[1], mu[2], mu[3], mu[4], mu[5], mu[6], mu[7],

@@ -763,6 +763,14 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drtab); cudaFree(p->drun); cudaFree(p->dmse);
         cudaFree(p->dkeys); cudaFree(p->dlab); cudaFree(p->dt_batch); cudaFree(p->dX_batch);
         if (p->gexec) cudaGraphExecDestroy(p->gexec);
+        if (p->copy_out) cudaStreamSynchronize(p->copy_out);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(p->dasync_in[i]); cudaFree(p->dasync_out[i]);
+            for (cudaEvent_t e : {p->ev_in[i], p->ev_comp[i], p->ev_out[i]})
+                if (e) cudaEventDestroy(e);
+        }
+        if (p->copy_in) cudaStreamDestroy(p->copy_in);
+        if (p->copy_out) cudaStreamDestroy(p->copy_out);
         for (auto &pair : p->ev)
             for (auto &e : pair)
                 if (e) cudaEventDestroy(e);
@@ -947,6 +955,64 @@ bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_
     BF_CUDA(cudaMemcpyAsync(out_host, p->dhost_out, bytes, cudaMemcpyDeviceToHost, s));
     BF_CUDA(cudaStreamSynchronize(s));
     return st;
+}
+
+// Pipelined frames: H2D of frame i+1 and D2H of frame i-1 run on two copy
+// streams while frame i computes on the caller's stream. Device slots alternate by call parity;
+// events order every reuse: the H2D into slot s waits for the compute that last read it, the compute
+// writing output slot s waits for the D2H that last read it.
+bf_status_t bf_vec_filter_host_async(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {
+    Nvtx nvtx_("bfvec:filter_host_async");
+    if (!valid_plan(p) || !f_host || !out_host) return BF_E_ARG;
+    if (p->device < 0 || !p->sampled) return BF_E_STATE;
+    const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
+    if (!p->copy_in) {
+        BF_CUDA(cudaStreamCreateWithFlags(&p->copy_in, cudaStreamNonBlocking));
+        BF_CUDA(cudaStreamCreateWithFlags(&p->copy_out, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            BF_CUDA(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming));
+            BF_CUDA(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
+            BF_CUDA(cudaEventCreateWithFlags(&p->ev_out[i], cudaEventDisableTiming));
+        }
+    }
+    if (p->dasync_bytes < bytes) {
+        BF_CUDA(cudaStreamSynchronize(p->copy_out));   // no frame in flight uses the old slots
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(p->dasync_in[i]); cudaFree(p->dasync_out[i]);
+            p->dasync_in[i] = p->dasync_out[i] = nullptr;
+        }
+        p->dasync_bytes = 0;
+        for (int i = 0; i < 2; ++i) {
+            BF_CUDA(cudaMalloc(&p->dasync_in[i], bytes));
+            BF_CUDA(cudaMalloc(&p->dasync_out[i], bytes));
+        }
+        p->dasync_bytes = bytes;
+        p->async_calls = 0;
+    }
+    cudaStream_t s = S(stream);
+    const int slot = (int)(p->async_calls & 1);
+    const bool reuse = p->async_calls >= 2;
+    if (reuse) BF_CUDA(cudaStreamWaitEvent(p->copy_in, p->ev_comp[slot], 0));   // frame i-2 read the slot
+    BF_CUDA(cudaMemcpyAsync(p->dasync_in[slot], f_host, bytes, cudaMemcpyHostToDevice, p->copy_in));
+    BF_CUDA(cudaEventRecord(p->ev_in[slot], p->copy_in));
+    BF_CUDA(cudaStreamWaitEvent(s, p->ev_in[slot], 0));
+    if (reuse) BF_CUDA(cudaStreamWaitEvent(s, p->ev_out[slot], 0));   // frame i-2's output was copied out
+    bf_status_t st = filter_band(p, p->dasync_in[slot], p->H, 0, 0, p->H, p->dasync_out[slot], s);
+    if (st < 0) return st;
+    BF_CUDA(cudaEventRecord(p->ev_comp[slot], s));
+    BF_CUDA(cudaStreamWaitEvent(p->copy_out, p->ev_comp[slot], 0));
+    BF_CUDA(cudaMemcpyAsync(out_host, p->dasync_out[slot], bytes, cudaMemcpyDeviceToHost, p->copy_out));
+    BF_CUDA(cudaEventRecord(p->ev_out[slot], p->copy_out));
+    p->async_calls += 1;
+    p->last = p->copy_out;
+    return st;
+}
+
+bf_status_t bf_vec_host_sync(bf_vec_plan_t p) {
+    if (!valid_plan(p)) return BF_E_ARG;
+    if (p->device < 0) return BF_E_STATE;
+    if (p->copy_out) BF_CUDA(cudaStreamSynchronize(p->copy_out));
+    return BF_OK;
 }
 
 bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k1, float *PZ,

@@ -220,6 +220,35 @@ def test_sample_shards_sum_to_full():
         np.testing.assert_allclose(S_band.cpu().numpy(), plain[:d, b0:b0 + n] / plain[d, b0:b0 + n], rtol=1e-6)
 
 
+def test_filter_host_async_frames_bitwise():
+    """bf_vec_filter_host_async: five different frames enqueued back to back (copies of frame i+1 / i-1
+    overlapping frame i), then one bf_vec_host_sync: each frame's output equals bf_vec_filter_host
+    bit for bit (the alternating device slots are never overwritten while in use)."""
+    cfg = CONFIGS[2]
+    base = make_image(cfg)
+    frames = [np.ascontiguousarray(np.roll(base, 37 * i, axis=2)) for i in range(5)]
+    p = H.gpu_plan(cfg)
+    ref = [p.filter_host(torch.from_numpy(fr).pin_memory()).clone() for fr in frames]
+    fin = [torch.from_numpy(fr).pin_memory() for fr in frames]
+    outs = [torch.empty((cfg.d, cfg.H, cfg.W), dtype=torch.float32).pin_memory() for _ in frames]
+    s = torch.cuda.Stream()
+    for fr, o in zip(fin, outs):
+        p.filter_host_async(fr, o, stream=s)
+    p.host_sync()
+    for i, (o, r) in enumerate(zip(outs, ref)):
+        assert torch.equal(o, r), f"frame {i}"
+    # again, with a sync between every second frame and the default stream
+    outs2 = [torch.empty_like(o) for o in outs]
+    for i, (fr, o) in enumerate(zip(fin, outs2)):
+        p.filter_host_async(fr, o)
+        if i % 2:
+            p.host_sync()
+    p.host_sync()
+    for o, r in zip(outs2, ref):
+        assert torch.equal(o, r)
+    p.close()
+
+
 def test_filter_host_matches_device():
     cfg = CONFIGS[1]
     f_np = make_image(cfg)
