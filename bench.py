@@ -52,6 +52,10 @@ def parse(argv=None):
     ap.add_argument("--engine", type=int, default=0, help="0 truncated FIR (default), 1 recursive O(1) engine")
     ap.add_argument("--sigma", type=float, default=0.0, help="override the config's sigma_s (engine sweeps)")
     ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled (default)")
+    ap.add_argument("--persistent", type=int, default=-1,
+                    help="v6 kernel schedule: 1 auto (library default), 0 classic grid, 2 persistent")
+    ap.add_argument("--rec-store", type=int, default=-1,
+                    help="engine 1 tiled: 1 pass 1 stores the row blur for pass 2 (default), 0 recompute")
     return ap.parse_args(argv)
 
 
@@ -319,6 +323,10 @@ def run_ours(args, cfg):
         plan.set_option("engine", args.engine)
     if args.rec_impl >= 0:
         plan.set_option("rec_impl", args.rec_impl)
+    if args.rec_store >= 0:
+        plan.set_option("rec_store", args.rec_store)
+    if args.persistent >= 0:
+        plan.set_option("persistent", args.persistent)
     plan.sample_freqs()
 
     # this rank's work
@@ -485,7 +493,7 @@ def run_ours(args, cfg):
             "data": "synthetic",
             "config": config_dict(cfg, world, args.mode, l2=l2_note, tile_rows=plan.info("tile_rows"),
                                   engine=("recursive" if args.engine == 1 else "fir"),
-                                  groups=plan.info("groups")),
+                                  groups=plan.info("groups"), persistent=plan.info("last_persistent")),
             "mpix_per_s": cfg.H * cfg.W * args.steps / (ms_max / 1e3) / 1e6,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,

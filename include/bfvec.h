@@ -25,7 +25,13 @@
  *    (a cudaStream_t passed as void*; NULL = legacy default stream). Launch
  *    failures are reported as BF_E_CUDA by the call that launched.
  *  - A plan owns its device scratch (frequency table, partial sums,
- *    diagnostics). One plan must not be used from two streams concurrently.
+ *    diagnostics). Calls on one plan are ordered on the device even across
+ *    streams: a call on a stream other than the previous call's waits for the
+ *    previous call's work (an event recorded per call; skipped while the
+ *    caller captures the stream into its own graph, which then orders it).
+ *    Host-side, one plan must not be called from two threads at once.
+ *  - Outputs may start at any 4-byte-aligned address (vector stores are used
+ *    only when a row start is 16-byte aligned).
  *  - No exceptions cross the ABI; every function returns a bf_status_t
  *    (< 0 error, 0 ok, > 0 warning). On error no output is written.
  *  - There is no CPU fallback: if no sm_100 device is present the calls that
@@ -266,6 +272,12 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *   "value_range" nominal data range R used for the alias warning (default 255)
  *   "tile_rows"   force the row-tile height of the fused kernel (0 = auto)
  *   "groups"      force the number of sample groups (0 = auto)
+ *   "persistent"  v6 kernel (variants 4, 7): 1 (default) auto -- a persistent schedule (one CTA per
+ *                 SM, each an equal share of the (strip, pass, chunk) work line, possibly starting
+ *                 and ending mid-pass) when the cost model says it beats the (strip, tile, group)
+ *                 grid by > 0.5 % (CTA counts that are not a whole number of waves: config 2 +10 %,
+ *                 config 5 +1 %) and
+ *                 no "tile_rows" / "groups" is forced; 0 never; 2 always (where the work allows)
  *   "direct_rows" bf_vec_direct: output rows per CTA, 4, 8 or 16 (0 = auto: 16 unless the
  *                 image has fewer 16-row tiles than SMs)
  *   "variant"     fused-kernel variant: 0 auto (d <= 3: 4 where compiled, else 2, else 1;
@@ -305,6 +317,9 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 planes stay in shared memory; 0 staged -- a row pass and a
  *                 column pass through HBM scratch. Same arithmetic, results equal to fp32
  *                 rounding (both gated against the oracle).
+ *   "rec_store"   engine 1, tiled: 1 pass 1 stores its exact row blur (2(d+1) fp32 planes per
+ *                 sample in flight) and pass 2 reads it instead of recomputing it; 0 (default)
+ *                 recompute (measured 2 % faster on config 5)
  *   "rec_batch"   engine 1: samples per batch (0 = auto: at most 256 and 40 % of the free
  *                 device memory, and for the tiled engine at most max(16 samples, 4 GiB of
  *                 summaries); each sample in flight holds, staged, 5 (d+1) fp32 planes of H x W

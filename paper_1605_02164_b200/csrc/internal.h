@@ -42,6 +42,13 @@ struct alignas(64) FusedArgs {
     // + (row - owner * p2p_rpb) * W + x, over NVLink while other CTAs are still computing.
     float *peer[8];
     int p2p_world, p2p_rank, p2p_rpb;
+    // persistent schedule (v6 kernel only; null = one (strip, tile, group) per CTA): CTA c runs the
+    // items [item_off[c], item_off[c+1]); item = {strip, u_begin, u_end, slot | zero_from << 16}
+    // over the strip's work line u = pass * nch_full + chunk (full-height passes of SP samples,
+    // chunks of KB rows), so every CTA gets the same number of chunk-steps
+    const int4 *items;
+    const int *item_off;
+    int nch_full;
 };
 
 struct PadMu {
@@ -141,6 +148,8 @@ struct RecTArgs {
     float2 *Eh, *Bh;      // (ns, 2(d+1), 2, ntx, H): row tiles' causal end / anticausal start states
     float2 *Ev, *Bv;      // (ns, 2(d+1), 2, nty, W): the same for the column tiles
     float4 *UVh, *UVv;    // (ns, 2(d+1), 2, H) / (.., W): line states (u_{-1}, v_n)
+    float *rbg;           // (ns, 2(d+1), H, W) row-blurred planes written by pass 1 and read by pass 2
+                          // (option "rec_store" = 1), or null: pass 2 recomputes the row blur
     RecTabs th, tv;
 };
 cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s);
@@ -186,6 +195,15 @@ struct bf_vec_plan_s {
     int force_tile_rows = 0;
     int force_groups = 0;
     int force_direct_rows = 0; // exact filter: output rows per CTA (0 auto, 4, 8, 16)
+    int persistent = 1;        // v6 kernel: 0 (strip, tile, group) grid, 1 auto, 2 force the persistent schedule
+    // cached persistent schedule: key, device item table, slots (groups) it needs
+    long long pers_key[5] = {-1, -1, -1, -1, -1};
+    int4 *ditems = nullptr;
+    int *ditem_off = nullptr;
+    size_t ditems_cap = 0, ditem_off_cap = 0;
+    int pers_groups = 0, pers_items = 0, pers_ctas = 0, last_persistent = 0;
+    int rec_store = 0;         // tiled recursive engine: 1 = pass 1 stores the row blur for pass 2 (measured
+                               // 2 % slower on config 5: pass 2 is not bound by the recomputed row blur)
     int force_variant = 0;     // 0 auto, 1 v3 (smem ring), 2 v4 (TMEM ring)
     int spatial = 0;           // spatial taps: 0 Gaussian (Eq. (1)), 1 box, 2 hat (reading R15)
     int engine = 0;            // 0 truncated FIR (Eq. (1) window), 1 recursive Deriche (reading R16)
@@ -245,6 +263,11 @@ struct bf_vec_plan_s {
     long long async_calls = 0;
     float mu[8];
     cudaStream_t last = nullptr;
+    // cross-stream ordering of the plan's shared scratch (StreamOrder in plan.cu): the event
+    // recorded after the last call and the stream it was recorded on
+    cudaEvent_t order_ev = nullptr;
+    cudaStream_t order_stream = nullptr;
+    bool order_recorded = false;
     // last schedule
     int last_tile_rows = 0, last_groups = 0;
     long long last_ctas = 0;

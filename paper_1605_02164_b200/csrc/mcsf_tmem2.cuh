@@ -42,8 +42,14 @@ struct CfgT2 {
     static constexpr int WIN = TX + 2 * R;
     static constexpr int MS = cs_stride(WIN);
     static constexpr int A = round_up(KB + 2 * R, 16);
-    static constexpr int HROWS = A + KB;
-    static constexpr int RING = A + KB - R + (MW_ > 0 ? 2 * SH : 0);   // modulators run <= 2 sub-steps ahead
+    // OV (pass overlap, where TMEM holds it: 2 samples x 2 x 2A columns <= 512, i.e. R <= 24): the
+    // ring holds 2A rows, so the producers fill the next pass's first A rows while the consumers
+    // still read the last chunk of the current one (its window ends A rows before the new rows'
+    // slots); every chunk then waits only for the consumers' chunk q-2. Without OV the first chunk
+    // of a pass waits for the whole previous pass (A + KB rows).
+    static constexpr bool OV = SP * 2 * (2 * A) <= 512;
+    static constexpr int HROWS = OV ? 2 * A : A + KB;
+    static constexpr int RING = HROWS - R + (MW_ > 0 ? 2 * SH : 0);   // modulators run <= 2 sub-steps ahead
     static constexpr int NIN = 8 + 2 * R;
     static constexpr int RCOLS = 2 * HROWS;                 // TMEM columns per ring
     static constexpr int TCOLS = (SP * RCOLS <= 32) ? 32 : (SP * RCOLS <= 64) ? 64 : (SP * RCOLS <= 128) ? 128
@@ -212,6 +218,112 @@ __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0
     }
 }
 
+// One pass over (part of) a strip: what every warp role needs to walk the same sequence of passes.
+struct PassDesc {
+    int x0;        // first column of the strip
+    int k, np;     // first sample (row of the t table) and samples in this pass (<= SP)
+    int cb, nch;   // first chunk of the tile and chunks in this pass
+    int prow;      // padded (tensor-map) row of H-row 0 of this pass
+    int ty0, ty1;  // output rows of the tile (image coordinates)
+    int slot, img; // partial-sum slot (sample group) and image of the batch
+    int ip;        // pass index within the item
+    int cb0;       // first chunk of the item's first pass
+    bool last;     // last pass of the item
+};
+
+// The pass sequence of one CTA: either the classic (strip, tile, group) of blockIdx -- passes of SP
+// samples over the whole tile -- or the items of the persistent schedule (FusedArgs::items).
+template <class C>
+struct PassIter {
+    const FusedArgs &a;
+    // classic
+    int x0, img, ty0, ty1, gk0, gk1, nch, prow0, g;
+    // persistent
+    int it, it_end, x, ub, ue, p, pe;
+    int pass;
+    __device__ explicit PassIter(const FusedArgs &a_) : a(a_) {
+        if (a.items) {
+            it = a.item_off[blockIdx.x];
+            it_end = a.item_off[blockIdx.x + 1];
+            load_item();
+        } else {
+            x0 = blockIdx.x * C::TX;
+            img = a.tiles_per_img ? (int)blockIdx.y / a.tiles_per_img : 0;     // image of the batch
+            const int tile = a.tiles_per_img ? (int)blockIdx.y % a.tiles_per_img : (int)blockIdx.y;
+            ty0 = a.out_row0 + tile * a.tile_rows;
+            ty1 = min(ty0 + a.tile_rows, a.out_row0 + a.out_rows);
+            g = blockIdx.z;
+            const int ns = a.k1 - a.k0;
+            // sample range of group g: a slice of [k0, k1), or -- realisation batching (gstride > 0,
+            // bf_vec_mse_sweep) -- the same [k0, k1) of realisation g's draws at t rows g * gstride + k
+            gk0 = a.gstride ? a.k0 + g * a.gstride : a.k0 + (int)((long long)ns * g / a.groups);
+            gk1 = a.gstride ? a.k1 + g * a.gstride : a.k0 + (int)((long long)ns * (g + 1) / a.groups);
+            nch = (ty1 - ty0 + C::KB - 1) / C::KB;
+            prow0 = img * a.img_prows + (ty0 - a.out_row0);
+            pass = 0;
+        }
+    }
+    __device__ void load_item() {
+        if (it >= it_end) return;
+        const int4 e = a.items[it];
+        x = e.x;
+        ub = e.y;
+        ue = e.z;
+        p = ub / a.nch_full;
+        pe = (ue - 1) / a.nch_full;
+        pass = 0;
+    }
+    __device__ bool valid() const { return a.items ? it < it_end : gk0 + pass * C::SP < gk1; }
+    __device__ PassDesc get() const {
+        PassDesc d;
+        if (a.items) {
+            const int nf = a.nch_full;
+            d.x0 = x * C::TX;
+            d.k = a.k0 + p * C::SP;
+            d.np = min(C::SP, a.k1 - d.k);
+            d.cb = (pass == 0) ? ub % nf : 0;
+            const int ce = (p == pe) ? (ue - 1) % nf + 1 : nf;
+            d.nch = ce - d.cb;
+            d.prow = d.cb * C::KB;
+            d.ty0 = a.out_row0;
+            d.ty1 = a.out_row0 + a.out_rows;
+            d.slot = a.items[it].w & 0xFFFF;
+            d.img = 0;
+            d.ip = pass;
+            d.cb0 = ub % nf;
+            d.last = p == pe;
+        } else {
+            d.x0 = x0;
+            d.k = gk0 + pass * C::SP;
+            d.np = min(C::SP, gk1 - d.k);
+            d.cb = 0;
+            d.nch = nch;
+            d.prow = prow0;
+            d.ty0 = ty0;
+            d.ty1 = ty1;
+            d.slot = g;
+            d.img = img;
+            d.ip = pass;
+            d.cb0 = 0;
+            d.last = d.k + C::SP >= gk1;
+        }
+        return d;
+    }
+    __device__ void advance() {
+        ++pass;
+        if (a.items && p++ == pe) {
+            ++it;
+            load_item();
+        }
+    }
+};
+
+// H-rows a pass streams: the first chunk's A (its 2R-row halo) and KB per further chunk
+template <class C>
+__device__ __forceinline__ int pass_rows(const PassDesc &d) {
+    return C::A + (d.nch - 1) * C::KB;
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_constant__ FusedArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -238,20 +350,6 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int x0 = blockIdx.x * C::TX;
-    const int img = a.tiles_per_img ? (int)blockIdx.y / a.tiles_per_img : 0;     // image of the batch
-    const int tile = a.tiles_per_img ? (int)blockIdx.y % a.tiles_per_img : (int)blockIdx.y;
-    const int ty0 = a.out_row0 + tile * a.tile_rows;
-    const int ty1 = min(ty0 + a.tile_rows, a.out_row0 + a.out_rows);
-    const int g = blockIdx.z;
-    const int ns = a.k1 - a.k0;
-    // sample range of group g: a slice of [k0, k1), or -- realisation batching (gstride > 0,
-    // bf_vec_mse_sweep) -- the same [k0, k1) of realisation g's draws at t rows g * gstride + k
-    const int gk0 = a.gstride ? a.k0 + g * a.gstride : a.k0 + (int)((long long)ns * g / a.groups);
-    const int gk1 = a.gstride ? a.k1 + g * a.gstride : a.k0 + (int)((long long)ns * (g + 1) / a.groups);
-    const int nchunks = (ty1 - ty0 + C::KB - 1) / C::KB;
-    const int rows_per_pass = C::A + (nchunks - 1) * C::KB;   // multiple of 16
-    const int prow0 = img * a.img_prows + (ty0 - a.out_row0);
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(taddr_s)),
@@ -276,7 +374,8 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tbase = *taddr_s;
 
-    if (gk0 < gk1) {
+    const PassIter<C> pit(a);   // this CTA's passes (every role walks the same sequence)
+    if (pit.valid()) {
         if (tid < C::NA) {
             // ============================ PRODUCER ============================
             const int ta = tid;
@@ -286,20 +385,24 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
             const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16) + (uint32_t)(sw * C::RCOLS);
             uint32_t tparity = 0;
             int buf = 0, it = 0;
-            if (C::MW == 0 && ta == 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0, C::TMA_BYTES);
-            int q = 0;
-            for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
-                const int np = min(C::SP, gk1 - k);
+            PassIter<C> pi = pit;
+            if (C::MW == 0 && ta == 0) {
+                const PassDesc d0 = pi.get();
+                tma_load_3d(fbuf, &a.tmap, tma_bar, 0, d0.x0, d0.prow, C::TMA_BYTES);
+            }
+            int q = 0, gs = 0;   // chunk counter, H-row counter at the start of the pass
+            for (; pi.valid(); pi.advance()) {
+                const PassDesc pd = pi.get();
+                const int np = pd.np, k = pd.k, nchunks = pd.nch;
                 float tk[2][C::D];
 #pragma unroll
                 for (int s = 0; s < 2; ++s)
 #pragma unroll
                     for (int c = 0; c < C::D; ++c)
                         tk[s][c] = (c < a.d && s < np) ? __ldg(a.t + (long long)(k + s) * a.d + c) : 0.f;
-                const int gs = pass * rows_per_pass;
                 for (int ci = 0; ci < nchunks; ++ci, ++q) {
                     const bool first_c = (ci == 0);
-                    if (first_c) {
+                    if (first_c && !C::OV) {
                         if (q >= 1) mbar_wait(&empty[(q - 1) & 1], ((q - 1) >> 1) & 1);
                     } else if (q >= 2) {
                         mbar_wait(&empty[q & 1], ((q - 2) >> 1) & 1);
@@ -320,8 +423,16 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                                 int nu = -1;
                                 if (s0 + C::SH < n_new) nu = u_begin + s0 + C::SH;
                                 else if (ci + 1 < nchunks) nu = C::A + ci * C::KB;
-                                else if (k + C::SP < gk1) nu = 0;
-                                if (nu >= 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0 + nu, C::TMA_BYTES);
+                                if (nu >= 0) {
+                                    tma_load_3d(fbuf, &a.tmap, tma_bar, 0, pd.x0, pd.prow + nu, C::TMA_BYTES);
+                                } else {   // first box of the next pass, if any
+                                    PassIter<C> nx = pi;
+                                    nx.advance();
+                                    if (nx.valid()) {
+                                        const PassDesc nd = nx.get();
+                                        tma_load_3d(fbuf, &a.tmap, tma_bar, 0, nd.x0, nd.prow, C::TMA_BYTES);
+                                    }
+                                }
                             }
                         } else {
                             mbar_wait(&gfull[buf], (it >> 1) & 1);   // the modulators filled G[buf]
@@ -375,6 +486,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                         }
                     }
                 }
+                gs += pass_rows<C>(pd);
             }
         } else if (tid >= C::NA + C::NB) {
             // ============================ MODULATORS (MW > 0) =================
@@ -385,16 +497,21 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                 const int tm = tid - C::NA - C::NB;
                 uint32_t tparity = 0;
                 int buf = 0, it = 0;
-                if (tm == 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0, C::TMA_BYTES);
-                for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
-                    const int np = min(C::SP, gk1 - k);
+                PassIter<C> pi = pit;
+                if (tm == 0) {
+                    const PassDesc d0 = pi.get();
+                    tma_load_3d(fbuf, &a.tmap, tma_bar, 0, d0.x0, d0.prow, C::TMA_BYTES);
+                }
+                int gs = 0;
+                for (; pi.valid(); pi.advance()) {
+                    const PassDesc pd = pi.get();
+                    const int np = pd.np, k = pd.k, nchunks = pd.nch;
                     float tk[2][C::D];
 #pragma unroll
                     for (int s = 0; s < 2; ++s)
 #pragma unroll
                         for (int c = 0; c < C::D; ++c)
                             tk[s][c] = (c < a.d && s < np) ? __ldg(a.t + (long long)(k + s) * a.d + c) : 0.f;
-                    const int gs = pass * rows_per_pass;
                     for (int ci = 0; ci < nchunks; ++ci) {
                         const bool first_c = (ci == 0);
                         const int u_begin = first_c ? 0 : C::A + (ci - 1) * C::KB;
@@ -414,12 +531,21 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                                 int nu = -1;
                                 if (s0 + C::SH < n_new) nu = u_begin + s0 + C::SH;
                                 else if (ci + 1 < nchunks) nu = C::A + ci * C::KB;
-                                else if (k + C::SP < gk1) nu = 0;
-                                if (nu >= 0) tma_load_3d(fbuf, &a.tmap, tma_bar, 0, x0, prow0 + nu, C::TMA_BYTES);
+                                if (nu >= 0) {
+                                    tma_load_3d(fbuf, &a.tmap, tma_bar, 0, pd.x0, pd.prow + nu, C::TMA_BYTES);
+                                } else {   // first box of the next pass, if any
+                                    PassIter<C> nx = pi;
+                                    nx.advance();
+                                    if (nx.valid()) {
+                                        const PassDesc nd = nx.get();
+                                        tma_load_3d(fbuf, &a.tmap, tma_bar, 0, nd.x0, nd.prow, C::TMA_BYTES);
+                                    }
+                                }
                             }
                             mbar_arrive(&gfull[buf]);
                         }
                     }
+                    gs += pass_rows<C>(pd);
                 }
             }
         } else {
@@ -431,28 +557,32 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
             const int h = (warp - C::NA / 32) >> 2;
             const int H0 = h * C::OR;
             const uint32_t tq = tbase + ((uint32_t)(32 * p) << 16);
-            const int x = x0 + lane;
             const bool active = p < C::NP;
-            const bool xok = x < a.W;
             const long long plane_out = (long long)a.out_rows * a.W;
             const int plane = (p == 0) ? C::D : p - 1;
-            float *pzp = a.pz + img * a.img_pz + ((long long)g * (C::D + 1) + plane) * plane_out + x;
             constexpr int OR = C::OR;
             constexpr int LR = (OR == 16) ? 16 : 8;                  // ring rows per TMEM load
             constexpr int JB1 = (OR - 1 + 2 * C::R) / LR + 1;        // loads per window
-            int q = 0;
-            for (int k = gk0, pass = 0; k < gk1; k += C::SP, ++pass) {
-                const int np = min(C::SP, gk1 - k);
-                const bool first_k = (k == gk0);
-                const int gs = pass * rows_per_pass;
+            PassIter<C> pi = pit;
+            int q = 0, gs = 0;
+            for (; pi.valid(); pi.advance()) {
+                const PassDesc pd = pi.get();
+                const int np = pd.np, nchunks = pd.nch, ty1 = pd.ty1;
+                const int x = pd.x0 + lane;
+                const bool xok = x < a.W;
+                float *pzp = a.pz + pd.img * a.img_pz + ((long long)pd.slot * (C::D + 1) + plane) * plane_out + x;
                 for (int ci = 0; ci < nchunks; ++ci, ++q) {
-                    const int cy = ty0 + ci * C::KB + H0;
+                    // this item's first visit of the chunk starts its partial sum (the item's first
+                    // pass covers chunks cb0.., its second pass the chunks before cb0)
+                    const int cabs = pd.cb + ci;
+                    const bool first = pd.ip == 0 || (pd.ip == 1 && cabs < pd.cb0);
+                    const int cy = pd.ty0 + cabs * C::KB + H0;
                     float *dst = pzp + (long long)(cy - a.out_row0) * a.W;
                     float tot[OR];
 #pragma unroll
                     for (int o = 0; o < OR; ++o) {
                         const bool ok = active && xok && (cy + o < ty1);
-                        tot[o] = (!first_k && ok) ? dst[(long long)o * a.W] : 0.f;
+                        tot[o] = (!first && ok) ? dst[(long long)o * a.W] : 0.f;
                     }
                     mbar_wait(&full[q & 1], (q >> 1) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -506,7 +636,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     mbar_arrive(&empty[q & 1]);
                     if (active && xok) {
-                        if (a.p2p_world > 0 && k + C::SP >= gk1) {
+                        if (a.p2p_world > 0 && pd.last) {
                             // last pass of the group: the finished partial goes to the band owner's
                             // receive slot (peer memory over NVLink), not back to the local tile
 #pragma unroll
@@ -515,7 +645,7 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                                 if (row < ty1) {
                                     const int owner = row / a.p2p_rpb;
                                     float *slot = a.peer[owner] +
-                                                  ((long long)(a.p2p_rank * a.groups + g) * (C::D + 1) + plane) *
+                                                  ((long long)(a.p2p_rank * a.groups + pd.slot) * (C::D + 1) + plane) *
                                                       a.p2p_rpb * a.W;
                                     slot[(long long)(row - owner * a.p2p_rpb) * a.W + x] = tot[o];
                                 }
@@ -527,6 +657,28 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                         }
                     }
                 }
+                if (a.items && pd.last && active && xok) {
+                    // persistent schedule, end of an item: the slot's rows this item never visited
+                    // (it covered less than a whole pass) and -- for the strip's last item -- the
+                    // slots no CTA uses for this strip are zeroed, so the normaliser can sum all
+                    // a.groups slots of every strip
+                    const int nf = a.nch_full;
+                    const int total = pi.ue - pi.ub, c0 = pi.ub % nf;
+                    const int zero_from = a.items[pi.it].w >> 16;
+                    auto zero_rows = [&](int z, int c) {
+                        float *zp = a.pz + ((long long)z * (C::D + 1) + plane) * plane_out + x;
+                        for (int o = 0; o < OR; ++o) {
+                            const int row = pd.ty0 + c * C::KB + H0 + o;
+                            if (row < ty1) zp[(long long)(row - a.out_row0) * a.W] = 0.f;
+                        }
+                    };
+                    for (int c = 0; c < nf; ++c) {
+                        if (total < nf && (c - c0 + nf) % nf >= total) zero_rows(pd.slot, c);
+                        if (zero_from > 0)
+                            for (int z = zero_from; z < a.groups; ++z) zero_rows(z, c);
+                    }
+                }
+                gs += pass_rows<C>(pd);
             }
         }
     }

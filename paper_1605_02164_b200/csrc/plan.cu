@@ -24,6 +24,42 @@ inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 // timeline of a multi-GPU run shows each rank's phases by name (`ncu --nvtx --nvtx-include
 // "bfvec:filter/"` selects the kernels of one phase). Header-only NVTX3: a no-op unless a tool
 // is attached.
+// Calls on one plan share its scratch (padded input, partial planes, summaries). A call on a stream
+// other than the previous call's first waits (on the device) for the previous call's work, so one
+// plan may be driven from several streams without racing on that scratch (found by the checked
+// build's timing: an eager call on the legacy stream overlapping the next call on a non-blocking
+// stream). Skipped while the stream is being captured by the caller (their graph orders it).
+struct StreamOrder {
+    bf_vec_plan_t p;
+    cudaStream_t s;
+    bool active = false;
+    StreamOrder(bf_vec_plan_t p_, cudaStream_t s_) : p(p_), s(s_) {
+        if (!p || p->device < 0) return;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+            cudaGetLastError();
+            return;
+        }
+        if (!p->order_ev && cudaEventCreateWithFlags(&p->order_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            p->order_ev = nullptr;
+            return;
+        }
+        if (p->order_recorded && p->order_stream != s) cudaStreamWaitEvent(s, p->order_ev, 0);
+        active = true;
+    }
+    ~StreamOrder() {
+        if (!active) return;
+        if (cudaEventRecord(p->order_ev, s) == cudaSuccess) {
+            p->order_stream = s;
+            p->order_recorded = true;
+        }
+        cudaGetLastError();
+    }
+    StreamOrder(const StreamOrder &) = delete;
+    StreamOrder &operator=(const StreamOrder &) = delete;
+};
+
 struct Nvtx {
     explicit Nvtx(const char *name) { nvtxRangePushA(name); }
     ~Nvtx() { nvtxRangePop(); }
@@ -329,6 +365,91 @@ struct RealBatch {
     int groups, stride;
 };
 
+// Persistent schedule for the v6 kernel (FusedArgs::items): one CTA per SM slot, each taking an
+// equal share of the work line (strip, pass, chunk) -- a contiguous range that may start and end
+// mid-pass -- instead of whole (strip, tile, sample group) CTAs, whose count rarely divides into
+// whole waves (config 2: 128 CTAs on 148 SMs). A CTA's range splits into one item per strip it
+// touches; the items of a strip write consecutive partial slots. Used when the cost model (chunk
+// steps incl. the A/KB-chunk pipeline fill per pass) beats the classic grid by > 0.5 %.
+// Returns the slot count (groups) or 0 when the classic grid stays.
+int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int groups, cudaStream_t s) {
+    const KernelInfo &ki = p->kinfo;
+    if (p->persistent == 0 || (ki.variant != 4 && ki.variant != 7)) return 0;
+    // a forced (tile_rows, groups) schedule is honoured unless persistent = 2 forces this one
+    if (p->persistent == 1 && (p->force_groups > 0 || p->force_tile_rows > 0)) return 0;
+    const long long nx = (p->W + kTX - 1) / kTX;
+    const long long nf = (out_rows + ki.kb - 1) / ki.kb;
+    const long long P = (ns + ki.sp - 1) / ki.sp;
+    const long long nC = (long long)sm_count() * std::max(1, ki.occupancy);
+    const long long U = nx * P * nf;
+    if (U < 4 * nC) return 0;
+    const double fill = (double)((ki.kb + 2 * ki.R + 15) / 16 * 16) / ki.kb;   // A / KB chunk-times per pass
+    // classic grid: whole waves of CTAs, each ceil(samples / SP) passes over its tile
+    const long long ny = (out_rows + tile_rows - 1) / tile_rows;
+    const long long ctas = nx * ny * groups;
+    const long long waves = (ctas + nC - 1) / nC;
+    const long long gpass = ((ns + groups - 1) / groups + ki.sp - 1) / ki.sp;
+    const double t_classic = (double)waves * gpass * ((tile_rows + ki.kb - 1) / ki.kb + fill);
+    const double share = (double)U / nC;
+    const double t_pers = std::ceil(share) + (share / nf + 2.0) * fill;
+    // the model matches the measurements: config 2 predicted 0.91, measured 0.90 (kernel time);
+    // config 5 predicted 0.989, measured 0.989; config 3 predicted 1.003 (stays classic)
+    if (p->persistent == 1 && !(t_pers < 0.995 * t_classic)) return 0;
+    const long long key[5] = {nx, nf, P, nC, ki.variant};
+    if (std::equal(key, key + 5, p->pers_key)) return p->pers_groups;
+    std::vector<int4> items;
+    std::vector<int> off(nC + 1);
+    std::vector<int> cnt(nx, 0);
+    std::vector<int> last_item(nx, -1);
+    const long long per_strip = P * nf;
+    for (long long c = 0; c < nC; ++c) {
+        long long u0 = U * c / nC;
+        const long long u1 = U * (c + 1) / nC;
+        off[c] = (int)items.size();
+        while (u0 < u1) {
+            const long long x = u0 / per_strip;
+            const long long e = std::min(u1, (x + 1) * per_strip);
+            last_item[x] = (int)items.size();
+            items.push_back(make_int4((int)x, (int)(u0 - x * per_strip), (int)(e - x * per_strip), cnt[x]++));
+            u0 = e;
+        }
+    }
+    off[nC] = (int)items.size();
+    int G = 1;
+    for (long long x = 0; x < nx; ++x) G = std::max(G, cnt[x]);
+    if (G > 0xFFFF) return 0;
+    for (long long x = 0; x < nx; ++x)   // the strip's last item zeroes the slots no CTA uses for it
+        if (cnt[x] < G) items[last_item[x]].w |= cnt[x] << 16;
+    if (p->ditems_cap < items.size()) {
+        cudaFree(p->ditems);
+        p->ditems = nullptr;
+        p->ditems_cap = 0;
+        if (cudaMalloc(&p->ditems, sizeof(int4) * items.size()) != cudaSuccess) { cudaGetLastError(); return 0; }
+        p->ditems_cap = items.size();
+        p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
+    }
+    if (p->ditem_off_cap < off.size()) {
+        cudaFree(p->ditem_off);
+        p->ditem_off = nullptr;
+        p->ditem_off_cap = 0;
+        if (cudaMalloc(&p->ditem_off, sizeof(int) * off.size()) != cudaSuccess) { cudaGetLastError(); return 0; }
+        p->ditem_off_cap = off.size();
+        p->gen += 1;
+    }
+    // ordered before the launches that read it (the copy is synchronous; it runs once per schedule)
+    if (cudaStreamSynchronize(s) != cudaSuccess ||
+        cudaMemcpy(p->ditems, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->ditem_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    std::copy(key, key + 5, p->pers_key);
+    p->pers_groups = G;
+    p->pers_items = (int)items.size();
+    p->pers_ctas = (int)nC;
+    return G;
+}
+
 bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_row0, int out_row0,
                       int out_rows, int k0, int k1, cudaStream_t s, int *groups_out, const P2POut *p2p = nullptr,
                       const RealBatch *rb = nullptr, int nimg = 1) {
@@ -338,9 +459,26 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
     if (p2p) groups = p2p->slots;   // one receive slot per (rank, group) on every owner
     if (rb) groups = rb->groups;    // one realisation per group
     const KernelInfo &ki = p->kinfo;
+    // the persistent schedule: single images without peer stores or realisation batches
+    cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+    const bool capturing = cudaStreamIsCapturing(s, &capst) == cudaSuccess && capst != cudaStreamCaptureStatusNone;
+    cudaGetLastError();
+    int pers = 0;
+    if (!p2p && !rb && nimg == 1) {
+        const long long key_nf = (out_rows + ki.kb - 1) / ki.kb;
+        const long long key_P = (k1 - k0 + ki.sp - 1) / std::max(1, ki.sp);
+        const bool cached = p->pers_key[1] == key_nf && p->pers_key[2] == key_P &&
+                            p->pers_key[0] == (p->W + kTX - 1) / kTX && p->pers_key[4] == ki.variant;
+        // never allocate or copy while the stream is captured: only a cached schedule may be used
+        if (!capturing || cached) pers = plan_persistent(p, out_rows, k1 - k0, tile_rows, groups, s);
+        if (pers) {
+            groups = pers;
+            tile_rows = (out_rows + ki.kb - 1) / ki.kb * ki.kb;
+        }
+    }
     size_t img_pz = (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;   // partial floats per image
     bf_status_t st = ensure_pz(p, sizeof(float) * img_pz * nimg);
-    if (st == BF_E_CUDA && !p2p && !rb && refresh_free_memory(p)) {
+    if (st == BF_E_CUDA && !p2p && !rb && !pers && refresh_free_memory(p)) {
         // memory taken since the cached query: re-plan the groups against what is free now
         choose_schedule(p, out_rows, k1 - k0, &tile_rows, &groups, nimg);
         img_pz = (size_t)groups * (ki.D + 1) * out_rows * (size_t)p->W;
@@ -393,6 +531,13 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
         a.img_pz = (long long)img_pz;
     }
     dim3 grid((p->W + kTX - 1) / kTX, ny * nimg, groups);
+    if (pers) {
+        a.items = p->ditems;
+        a.item_off = p->ditem_off;
+        a.nch_full = (out_rows + ki.kb - 1) / ki.kb;
+        grid = dim3(p->pers_ctas, 1, 1);
+    }
+    p->last_persistent = pers ? 1 : 0;
     p->last_tile_rows = tile_rows;
     p->last_groups = groups;
     p->last_ctas = (long long)grid.x * grid.y * grid.z;
@@ -546,7 +691,8 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     // per sample in flight: row / column summaries (E, B) and line states
     const size_t sum_h = (size_t)NQ * 2 * ntx * p->H, sum_v = (size_t)NQ * 2 * nty * p->W;
     const size_t uv_h = (size_t)NQ * 2 * p->H, uv_v = (size_t)NQ * 2 * p->W;
-    const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v);
+    const size_t rb_per = p->rec_store ? sizeof(float) * (size_t)NQ * px : 0;   // stored row blur
+    const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v) + rb_per;
     int nb = 1, g = 1;
     bf_status_t st = BF_OK;
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -601,6 +747,7 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     a.Bv = a.Ev + (size_t)nb * sum_v;
     a.UVh = reinterpret_cast<float4 *>(a.Bv + (size_t)nb * sum_v);
     a.UVv = a.UVh + (size_t)nb * uv_h;
+    a.rbg = p->rec_store ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
     rec_axis(p->sigma_s, p->W, &a.row);
     rec_axis(p->sigma_s, p->H, &a.col);
     int slot = -1;
@@ -762,8 +909,13 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
         cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drtab); cudaFree(p->drun); cudaFree(p->dmse);
         cudaFree(p->dkeys); cudaFree(p->dlab); cudaFree(p->dt_batch); cudaFree(p->dX_batch);
+        cudaFree(p->ditems); cudaFree(p->ditem_off);
         if (p->gexec) cudaGraphExecDestroy(p->gexec);
         if (p->copy_out) cudaStreamSynchronize(p->copy_out);
+        if (p->order_ev) {
+            cudaEventSynchronize(p->order_ev);
+            cudaEventDestroy(p->order_ev);
+        }
         for (int i = 0; i < 2; ++i) {
             cudaFree(p->dasync_in[i]); cudaFree(p->dasync_out[i]);
             for (cudaEvent_t e : {p->ev_in[i], p->ev_comp[i], p->ev_out[i]})
@@ -780,6 +932,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
 
 bf_status_t bf_vec_sample_freqs(bf_vec_plan_t p, void *stream) {
     Nvtx nvtx_("bfvec:sample");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p)) return BF_E_ARG;
     bf_status_t st = ensure_device(p);
     if (st != BF_OK) return st;
@@ -901,6 +1054,7 @@ bf_status_t filter_graph(bf_vec_plan_t p, const float *f, float *out, cudaStream
 
 bf_status_t bf_vec_filter(bf_vec_plan_t p, const float *f, float *out, void *stream) {
     Nvtx nvtx_("bfvec:filter");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
     if (p->device < 0) return BF_E_STATE;
     cudaStream_t s = S(stream);
@@ -916,6 +1070,7 @@ bf_status_t bf_vec_filter(bf_vec_plan_t p, const float *f, float *out, void *str
 
 bf_status_t bf_vec_filter_batch(bf_vec_plan_t p, const float *f, float *out, int nimg, void *stream) {
     Nvtx nvtx_("bfvec:filter_batch");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f || !out || f == out || nimg < 1) return BF_E_ARG;
     if (p->device < 0 || !p->sampled) return BF_E_STATE;
     if (p->engine != 0 || p->lab) return BF_E_UNSUPPORTED;
@@ -937,6 +1092,7 @@ bf_status_t bf_vec_filter_batch(bf_vec_plan_t p, const float *f, float *out, int
 
 bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {
     Nvtx nvtx_("bfvec:filter_host");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f_host || !out_host) return BF_E_ARG;
     if (p->device < 0) return BF_E_STATE;
     const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
@@ -963,6 +1119,7 @@ bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_
 // writing output slot s waits for the D2H that last read it.
 bf_status_t bf_vec_filter_host_async(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {
     Nvtx nvtx_("bfvec:filter_host_async");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f_host || !out_host) return BF_E_ARG;
     if (p->device < 0 || !p->sampled) return BF_E_STATE;
     const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
@@ -1018,6 +1175,7 @@ bf_status_t bf_vec_host_sync(bf_vec_plan_t p) {
 bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k1, float *PZ,
                                   int rows_per_band, void *stream) {
     Nvtx nvtx_("bfvec:filter_partial");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f || !PZ) return BF_E_ARG;
     if (k0 < 0 || k1 > p->M || k0 > k1 || rows_per_band < 1 || rows_per_band > p->H) return BF_E_ARG;
     if (p->device < 0 || !p->sampled) return BF_E_STATE;
@@ -1044,6 +1202,7 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k
 bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t p, const float *f, int k0, int k1, float *const *peer_slots,
                                       int world, int rank, int slots_per_rank, void *stream) {
     Nvtx nvtx_("bfvec:filter_partial_p2p");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f || !peer_slots) return BF_E_ARG;
     if (world < 1 || world > 8 || rank < 0 || rank >= world || slots_per_rank < 1) return BF_E_ARG;
     if (k0 < 0 || k1 > p->M || k1 - k0 < slots_per_rank) return BF_E_ARG;   // every group non-empty
@@ -1066,6 +1225,7 @@ bf_status_t bf_vec_filter_partial_p2p(bf_vec_plan_t p, const float *f, int k0, i
 bf_status_t bf_vec_normalize_slots(bf_vec_plan_t p, const float *slots, int nslots, int row0, int row1,
                                    float *out_band, void *stream) {
     Nvtx nvtx_("bfvec:normalize_slots");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !slots || !out_band || nslots < 1) return BF_E_ARG;
     if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
     if (p->device < 0 || !p->kinfo_ok || p->p2p_world < 1) return BF_E_STATE;
@@ -1087,6 +1247,7 @@ bf_status_t bf_vec_normalize_slots(bf_vec_plan_t p, const float *slots, int nslo
 bf_status_t bf_vec_normalize(bf_vec_plan_t p, const float *PZ_band, int row0, int row1, float *out_band,
                              void *stream) {
     Nvtx nvtx_("bfvec:normalize");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !PZ_band || !out_band) return BF_E_ARG;
     if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
     bf_status_t st = ensure_device(p);
@@ -1103,6 +1264,7 @@ bf_status_t bf_vec_normalize(bf_vec_plan_t p, const float *PZ_band, int row0, in
 bf_status_t bf_vec_filter_rows(bf_vec_plan_t p, const float *slab, int slab_row0, int slab_rows, int row0,
                                int row1, float *out_band, void *stream) {
     Nvtx nvtx_("bfvec:filter_rows");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !slab || !out_band) return BF_E_ARG;
     if (row0 < 0 || row1 > p->H || row0 >= row1) return BF_E_ARG;
     if (slab_row0 < 0 || slab_rows < 1 || slab_row0 + slab_rows > p->H) return BF_E_ARG;
@@ -1121,6 +1283,7 @@ bf_status_t bf_vec_filter_rows(bf_vec_plan_t p, const float *slab, int slab_row0
 
 bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *stream) {
     Nvtx nvtx_("bfvec:direct");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f || !out || f == out) return BF_E_ARG;
     if (p->r > kMaxR) return BF_E_UNSUPPORTED;
     bf_status_t st = ensure_device(p);
@@ -1162,6 +1325,7 @@ bf_status_t bf_vec_direct(bf_vec_plan_t p, const float *f, float *out, void *str
 bf_status_t bf_vec_mse_sweep(bf_vec_plan_t p, const float *f, const float *ref, int n_seeds, const uint64_t *seeds,
                              int n_t, const int *t_list, double *mse, void *stream) {
     Nvtx nvtx_("bfvec:mse_sweep");
+    StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
     if (!valid_plan(p) || !f || !ref || !seeds || !t_list || !mse || n_seeds < 1 || n_t < 1) return BF_E_ARG;
     for (int j = 0; j < n_t; ++j)
         if (t_list[j] < 1 || t_list[j] > p->M || (j > 0 && t_list[j] <= t_list[j - 1])) return BF_E_ARG;
@@ -1364,6 +1528,16 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         p->rec_impl = (int)v;
         return BF_OK;
     }
+    if (!std::strcmp(name, "persistent")) {
+        if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
+        p->persistent = (int)v;
+        return BF_OK;
+    }
+    if (!std::strcmp(name, "rec_store")) {
+        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        p->rec_store = (int)v;
+        return BF_OK;
+    }
     if (!std::strcmp(name, "rec_batch")) { if (v < 0) return BF_E_ARG; p->force_batch = (int)v; return BF_OK; }
     if (!std::strcmp(name, "spatial_kernel")) {
         if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
@@ -1396,7 +1570,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"sampler", p->sampler}, {"colorspace", p->lab},
+        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"rec_store", p->rec_store}, {"persistent", p->persistent}, {"last_persistent", p->last_persistent}, {"sampler", p->sampler}, {"colorspace", p->lab},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)

@@ -262,7 +262,9 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
     // entering states, software-pipelined: the row states of sample b are loaded during sample
     // b-1's column stage, the column states of sample b during its row stage
     St rl, rr, cl, cr;
-    if (MODE >= 1 && s0 < s1 && lane < Ly) get_states(a.Eh, a.Bh, a.UVh, a.th, s0, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
+    const bool rb_load = MODE == 2 && a.rbg != nullptr;   // pass 2 reads pass 1's row blur
+    if (MODE >= 1 && !rb_load && s0 < s1 && lane < Ly)
+        get_states(a.Eh, a.Bh, a.UVh, a.th, s0, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
     for (int b = s0; b < s1; ++b) {
         const int k = a.k0 + b;
         float tk[D];
@@ -299,14 +301,25 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
                 else summaries<false>(zp, Lx, xat, e, bb);
                 put_state(a.Eh, e, b, p, tx, y, NQ, a.ntx, H);
                 put_state(a.Bh, bb, b, p, tx, y, NQ, a.ntx, H);
-            } else {
+            } else if (!rb_load) {
                 float *r0 = rb + (2 * p * T + lane) * TP, *r1 = rb + ((2 * p + 1) * T + lane) * TP;
                 if (full) blur_segment<true>(a.row, T, xat, rl, rr, r0, r1);
                 else blur_segment<false>(a.row, Lx, xat, rl, rr, r0, r1);
             }
         }
         if (MODE == 0) continue;
-        if (b + 1 < s1 && lane < Ly)
+        if (rb_load && lane < Lx) {
+            // pass 1's exact row blur of this tile (planes 2p, 2p+1): lane = column, coalesced rows
+            const float *g0 = a.rbg + (((long long)b * NQ + 2 * p) * H + y0) * W + x0 + lane;
+            const float *g1 = g0 + (long long)H * W;
+            float *r0 = rb + 2 * p * T * TP + lane, *r1 = rb + (2 * p + 1) * T * TP + lane;
+#pragma unroll 8
+            for (int m = 0; m < Ly; ++m) {
+                r0[m * TP] = __ldg(g0 + (long long)m * W);
+                r1[m * TP] = __ldg(g1 + (long long)m * W);
+            }
+        }
+        if (!rb_load && b + 1 < s1 && lane < Ly)
             get_states(a.Eh, a.Bh, a.UVh, a.th, b + 1, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
         // the column stage of pair p reads only rb planes 2p, 2p+1 (written by this warp) and cs
         // (complete since the barrier after the modulation): a warp barrier suffices
@@ -317,6 +330,15 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
             const int x = x0 + lane;
             const float *c0 = rb + 2 * p * T * TP + lane, *c1 = rb + (2 * p + 1) * T * TP + lane;
             if (MODE == 1) {
+                if (a.rbg) {   // keep the exact row blur for pass 2 (lane = column: coalesced rows)
+                    float *g0 = a.rbg + (((long long)b * NQ + 2 * p) * H + y0) * W + x;
+                    float *g1 = g0 + (long long)H * W;
+#pragma unroll 8
+                    for (int m = 0; m < Ly; ++m) {
+                        g0[(long long)m * W] = c0[m * TP];
+                        g1[(long long)m * W] = c1[m * TP];
+                    }
+                }
                 auto xat = [&](int m) -> float2 { return f2(c0[m * TP], c1[m * TP]); };
                 St e, bb;
                 if (full) summaries<true>(zp + T, T, xat, e, bb);

@@ -126,6 +126,34 @@ def test_guard_bands_batch_and_lab():
     p.close()
 
 
+def test_one_plan_two_streams_is_ordered():
+    """One plan driven from the legacy default stream and a non-blocking stream back to back, no
+    host sync in between: the library orders the calls on the device (StreamOrder), so the shared
+    scratch is never raced (the checked build's slower kernels exposed the unordered case)."""
+    cfg = CONFIGS[2]
+    f = torch.from_numpy(make_image(cfg)).cuda()
+    g = f.flip(2).contiguous()
+    p = H.gpu_plan(cfg)
+    p.set_option("graph", 0)
+    rf = p.filter(f).clone()
+    rg = p.filter(g).clone()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    outs = []
+    for i in range(6):
+        o = torch.empty_like(f)
+        src = f if i % 2 == 0 else g
+        if i % 3 == 0:
+            p.filter(src, o)                 # legacy default stream
+        else:
+            p.filter(src, o, stream=s)       # non-blocking stream, no sync with the previous call
+        outs.append((o, rf if i % 2 == 0 else rg))
+    torch.cuda.synchronize()
+    for i, (o, r) in enumerate(outs):
+        assert torch.equal(o, r), f"call {i}"
+    p.close()
+
+
 def test_two_streams_two_plans_bitwise():
     """Two plans (different kernels: v6 at r = 15 and the recursive engine) on two streams, their
     launches interleaved so the kernels overlap on the device: each result equals its isolated run

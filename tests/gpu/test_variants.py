@@ -96,3 +96,54 @@ def test_variant1_d8_parity(case):
     res = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
     print(case, res)
     H.assert_gates(res)
+
+
+# The persistent schedule of the v6 kernel (option "persistent": one CTA per SM, each an equal share
+# of the (strip, pass, chunk) work line, items starting / ending mid-pass, per-strip slots, zeroed
+# unused rows and slots): forced on against the oracle, on shapes whose shares start mid-pass,
+# span several strips, cover less than one pass, and with odd sample counts (one-sample passes).
+@pytest.mark.parametrize("case", [(131, 77, 3, 5.0, 30, 17, 9, "full"), (70, 96, 3, 16.0, 40, 7, 2, "diag"),
+                                  (512, 70, 3, 2.0, 20, 9, 5, "diag"), (300, 200, 1, 3.3, 20, 6, 7, "full"),
+                                  (40, 33, 2, 8.0, 20, 5, 4, "full")])
+def test_persistent_schedule_parity(case):
+    cfg = _edge_cfg(case)
+    f = random_image(cfg.H, cfg.W, cfg.d, seed=cfg.seed, smooth=True)
+    Q, a, Y = H.oracle_draws(cfg)
+    S_o, P_o, Z_o = native.mcsf_full(f, Q, a, cfg.N, Y, cfg.sigma_s)
+    p = H.gpu_plan(cfg)
+    p.set_option("persistent", 2)
+    res = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
+    print(case, "persistent", p.info("last_persistent"), "groups", p.info("groups"), res)
+    H.assert_gates(res)
+    p.set_option("persistent", 0)
+    res0 = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
+    assert p.info("last_persistent") == 0
+    H.assert_gates(res0)
+
+
+def test_persistent_config2_default_and_graph():
+    """Config 2 picks the persistent schedule by default (its 128 classic CTAs leave 20 SMs idle);
+    the result passes the gates, repeats bitwise, and graph replay equals eager."""
+    import torch
+    cfg = CONFIGS[2]
+    f = make_image(cfg)
+    Q, a, Y = H.oracle_draws(cfg)
+    S_o, P_o, Z_o = native.mcsf_full(f, Q, a, cfg.N, Y, cfg.sigma_s)
+    p = H.gpu_plan(cfg)
+    S_g, P_g, Z_g = H.gpu_run(p, f)
+    assert p.info("last_persistent") == 1
+    H.assert_gates(H.gates(cfg, S_g, P_g, Z_g, S_o, P_o, Z_o))
+    fg = torch.from_numpy(f).cuda()
+    p.set_option("graph", 0)
+    e1 = p.filter(fg).clone()
+    e2 = p.filter(fg).clone()
+    assert torch.equal(e1, e2)
+    p.set_option("graph", 1)
+    s = torch.cuda.Stream()
+    out = torch.empty_like(fg)
+    with torch.cuda.stream(s):
+        for _ in range(4):
+            p.filter(fg, out)
+    s.synchronize()
+    assert p.info("graph_ready") == 1
+    assert torch.equal(out, e1)
