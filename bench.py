@@ -154,15 +154,16 @@ def measured_traffic(cfg, kernel, units, schedule):
     `ncu --set full` capture of this workload and launch schedule (profiles/r01_traffic.json),
     scaled by the launch's pixel-samples; None if no capture matches (the partial-sum traffic
     depends on the (tile_rows, groups) schedule)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
-            tab = json.load(fh)
-    except Exception:
-        return None
-    e = tab.get(f"{cfg.name}|{kernel}")
-    if not e or e.get("schedule") != schedule:
-        return None
-    return (e["dram_bytes_read"] + e["dram_bytes_write"]) * units / e["units"]
+    for name in ("r02_traffic.json", "r01_traffic.json"):   # newest capture first
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                tab = json.load(fh)
+        except Exception:
+            continue
+        e = tab.get(f"{cfg.name}|{kernel}")
+        if e and all(e.get("schedule", {}).get(k, 0) == v for k, v in schedule.items()):
+            return (e["dram_bytes_read"] + e["dram_bytes_write"]) * units / e["units"]
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -470,13 +471,17 @@ def run_ours(args, cfg):
                  else "rec_row_kernel+rec_col_kernel")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": measured_traffic(cfg, kname, units_per_launch,
-                                        {"tile_rows": plan.info("tile_rows"), "groups": plan.info("groups")}),
+                                        {"tile_rows": plan.info("tile_rows"), "groups": plan.info("groups"),
+                                         "persistent": plan.info("last_persistent")}),
+            # algorithmic bytes per launch: read f, write S (8 d B per output pixel)
+            "algorithmic_bytes": 8 * cfg.d * rows * cfg.W,
             "kernel": kname, "fused_ms_per_launch": fused_ms,
             "peak_source": f"FP32 pipe: 148 SM x 128 lanes x 2 flop x {mhz_max} MHz (sm_max)",
             "frac_at_run_clock": (achieved / fp32_peak_tflops(clocks["sm_mhz"])) if clocks.get("sm_mhz") else None,
             "flops_per_px_sample": (algorithmic_flops_per_px_sample(cfg.d, r) if args.engine == 0
                                     else recursive_flops_per_px_sample(cfg.d)),
             "fused_share_of_step": (fused_ns / 1e6) / ms if ms > 0 else None}
+    roof["traffic_ratio"] = (roof["traffic"] / roof["algorithmic_bytes"]) if roof["traffic"] else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

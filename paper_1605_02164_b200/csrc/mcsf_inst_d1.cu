@@ -8,9 +8,14 @@
 
 namespace bfvec {
 
-#define BFV_INSTANCES(X) X(1, 2, 64, 16, 16) X(1, 6, 64, 16, 16) X(1, 15, 64, 16, 16) X(1, 32, 64, 16, 16) X(1, 64, 64, 16, 16)
 #define BFV_TMEM2_INSTANCES(X) X(1, 6) X(1, 10) X(1, 15) X(1, 24) X(1, 30) X(1, 48)
+#ifdef BFVEC_COMPARISON_VARIANTS   // see mcsf_inst_d3.cu
+#define BFV_INSTANCES(X) X(1, 2, 64, 16, 16) X(1, 6, 64, 16, 16) X(1, 15, 64, 16, 16) X(1, 32, 64, 16, 16) X(1, 64, 64, 16, 16)
 #define BFV_TMEM_INSTANCES(X) X(1, 6) X(1, 15) X(1, 24) X(1, 32) X(1, 48)
+#else
+#define BFV_INSTANCES(X) X(1, 64, 64, 16, 16)
+#define BFV_TMEM_INSTANCES(X) X(1, 32)
+#endif
 
 // variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 4 force v5
 bool fused_select_d1(int r, int variant, KernelInfo *info) {

@@ -8,9 +8,14 @@
 
 namespace bfvec {
 
-#define BFV_INSTANCES(X) X(2, 6, 96, 16, 16) X(2, 15, 96, 16, 16) X(2, 32, 96, 16, 16) X(2, 64, 96, 16, 8)
 #define BFV_TMEM2_INSTANCES(X) X(2, 6) X(2, 10) X(2, 15) X(2, 24) X(2, 30) X(2, 48)
+#ifdef BFVEC_COMPARISON_VARIANTS   // see mcsf_inst_d3.cu
+#define BFV_INSTANCES(X) X(2, 6, 96, 16, 16) X(2, 15, 96, 16, 16) X(2, 32, 96, 16, 16) X(2, 64, 96, 16, 8)
 #define BFV_TMEM_INSTANCES(X) X(2, 6) X(2, 15) X(2, 24) X(2, 32) X(2, 48)
+#else
+#define BFV_INSTANCES(X) X(2, 64, 96, 16, 8)
+#define BFV_TMEM_INSTANCES(X) X(2, 32)
+#endif
 
 // variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 4 force v5
 bool fused_select_d2(int r, int variant, KernelInfo *info) {

@@ -8,8 +8,18 @@
 
 namespace bfvec {
 
+// The default build compiles only the instances the default selection can pick (build
+// weight): v3 for 48 < r <= 64, v4 for r <= 2 and r = 4 (no v6 instance as tight), v6 elsewhere.
+// -DBFVEC_COMPARISON_VARIANTS adds the comparison instances (v3 / v4 at every radius, variants 3,
+// 5, 6); forcing a variant that is not compiled falls back to the nearest compiled instance of it
+// (a padded radius: taps beyond r are zero) or the default order.
+#ifdef BFVEC_COMPARISON_VARIANTS
 #define BFV_INSTANCES(X) X(3, 2, 128, 16, 16) X(3, 4, 128, 16, 16) X(3, 6, 128, 16, 16) X(3, 10, 128, 16, 16) X(3, 15, 128, 16, 16) X(3, 24, 256, 16, 16) X(3, 30, 256, 16, 16) X(3, 48, 256, 16, 16) X(3, 64, 64, 8, 8)
 #define BFV_TMEM_INSTANCES(X) X(3, 2) X(3, 4) X(3, 6) X(3, 10) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
+#else
+#define BFV_INSTANCES(X) X(3, 64, 64, 8, 8)
+#define BFV_TMEM_INSTANCES(X) X(3, 2) X(3, 4)
+#endif
 #define BFV_TMEM2_INSTANCES(X) X(3, 3) X(3, 6) X(3, 10) X(3, 15) X(3, 24) X(3, 30) X(3, 48)
 
 // variant: 0 auto (v5 where compiled, else v4, else v3), 1 force v3, 2 force v4, 3 v4 with two
@@ -47,6 +57,7 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
         BFV_TMEM2_INSTANCES(BFV_FILLB)
 #undef BFV_FILLB
     }
+#ifdef BFVEC_COMPARISON_VARIANTS
     if (variant == 6 && bestT == 48) {   // v5c: modulation by the producer warps (comparison instance)
         fill_info_tmem2<CfgT2<3, 48, 2, 0>>(info);
         info->variant = 6;
@@ -62,6 +73,7 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
         info->variant = 3;
         return true;
     }
+#endif
     if (use_t) {
 #define BFV_FILLT(D_, R_) \
     if (R_ == bestT) fill_info_tmem<CfgT<D_, R_, 16>>(info);
@@ -80,9 +92,11 @@ bool fused_select_d3(int r, int variant, KernelInfo *info) {
 }
 
 cudaError_t fused_launch_d3(const KernelInfo &info, const FusedArgs &a, dim3 grid, cudaStream_t s) {
+#ifdef BFVEC_COMPARISON_VARIANTS
     if (info.variant == 3) return launch_tmem<CfgT<3, 48, 16, 2>>(a, grid, s);
     if (info.variant == 5) return launch_tmem2<CfgT2<3, 48, 1>>(a, grid, s);
     if (info.variant == 6) return launch_tmem2<CfgT2<3, 48, 2, 0>>(a, grid, s);
+#endif
     if (info.variant == 7) {
 #define BFV_LAUNCHB(D_, R_) \
     if (info.R == R_) return launch_tmem2<CfgT2<D_, R_, 2, 4, true>>(a, grid, s);

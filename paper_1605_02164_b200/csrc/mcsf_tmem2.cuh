@@ -185,6 +185,7 @@ __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0
                                           int *cstag = nullptr) {
     (void)cstag;
     constexpr int PER = (C::SH * C::WIN + NTH - 1) / NTH;
+    const int base = g0 % C::RING;   // ring row of the sub-step's row 0 (one modulo per call)
 #pragma unroll
     for (int i = 0; i < PER; ++i) {
         const int it = ta + i * NTH;
@@ -194,7 +195,8 @@ __device__ __forceinline__ void modulate2(int ta, const float *fbuf, float2 *gb0
         const float4 q = *reinterpret_cast<const float4 *>(fbuf + (row * C::WIN + j) * C::DP);
         const float fv[4] = {q.x, q.y, q.z, q.w};
         const bool inner = j >= C::R && j < C::R + C::TX;
-        const int rs = ((g0 + row) % C::RING) * C::TX + (j - C::R);
+        const int rr = base + row;   // row < SH <= RING: at most one wrap
+        const int rs = (rr >= C::RING ? rr - C::RING : rr) * C::TX + (j - C::R);
 #pragma unroll
         float2 th2 = make_float2(0.f, 0.f);   // both samples' phases, one FFMA2 per channel
 #pragma unroll
