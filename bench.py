@@ -309,11 +309,20 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BFVEC_BENCH_BACKEND=gloo: an orchestration check of the N > 1 code path on a box with fewer
+    # GPUs than ranks (ranks share devices round-robin; host collectives; NOT a timing). The
+    # driver's runs use NCCL, one rank per GPU.
+    backend = os.environ.get("BFVEC_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         comm = communicator_report(dist, dev, world)
     r = cfg.radius
     plan = Plan(cfg.H, cfg.W, cfg.d, cfg.sigma_s, cfg.C_array, cfg.N, cfg.M, cfg.seed,

@@ -43,7 +43,7 @@ struct alignas(64) FusedArgs {
     float *peer[8];
     int p2p_world, p2p_rank, p2p_rpb;
     // persistent schedule (v6 kernel only; null = one (strip, tile, group) per CTA): CTA c runs the
-    // items [item_off[c], item_off[c+1]); item = {strip, u_begin, u_end, slot | zero_from << 16}
+    // items [item_off[c], item_off[c+1]); item = {strip, u_begin, u_end, slot}
     // over the strip's work line u = pass * nch_full + chunk (full-height passes of SP samples,
     // chunks of KB rows), so every CTA gets the same number of chunk-steps
     const int4 *items;
@@ -92,9 +92,11 @@ cudaError_t launch_sampler_stratified(int M, int d, int N, uint64_t seed, const 
 // Epilogues (normalize.cu)
 cudaError_t launch_normalize_groups(const float *pz, int groups, int D, int d, int rows, int W,
                                     const float *mu, float *out, float *diag, float inv_m,
-                                    float z_floor, cudaStream_t s);
+                                    float z_floor, cudaStream_t s, const int *strip_slots = nullptr);
+// strip_slots (persistent schedule): slots written per 32-column strip; null = `groups` everywhere
 cudaError_t launch_finalize_partial(const float *pz, int groups, int D, int d, int rows, int W,
-                                    const float *mu, int rows_per_band, float *PZ, cudaStream_t s);
+                                    const float *mu, int rows_per_band, float *PZ, cudaStream_t s,
+                                    const int *strip_slots = nullptr);
 cudaError_t launch_normalize_raw(const float *PZ, int d, int rows, int W, float *out, float *diag,
                                  float inv_m, float z_floor, cudaStream_t s);
 cudaError_t launch_diag_reset(float *diag, cudaStream_t s);
@@ -200,6 +202,9 @@ struct bf_vec_plan_s {
     long long pers_key[5] = {-1, -1, -1, -1, -1};
     int4 *ditems = nullptr;
     int *ditem_off = nullptr;
+    int *dstrip_slots = nullptr;      // slots written per strip (the normaliser sums only those)
+    size_t dstrip_cap = 0;
+    const int *last_strip_slots = nullptr;   // of the last fused launch (null: classic grid)
     size_t ditems_cap = 0, ditem_off_cap = 0;
     int pers_groups = 0, pers_items = 0, pers_ctas = 0, last_persistent = 0;
     int rec_store = 0;         // tiled recursive engine: 1 = pass 1 stores the row blur for pass 2 (measured

@@ -289,7 +289,7 @@ struct PassIter {
             d.prow = d.cb * C::KB;
             d.ty0 = a.out_row0;
             d.ty1 = a.out_row0 + a.out_rows;
-            d.slot = a.items[it].w & 0xFFFF;
+            d.slot = a.items[it].w;
             d.img = 0;
             d.ip = pass;
             d.cb0 = ub % nf;
@@ -659,25 +659,19 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                         }
                     }
                 }
-                if (a.items && pd.last && active && xok) {
-                    // persistent schedule, end of an item: the slot's rows this item never visited
-                    // (it covered less than a whole pass) and -- for the strip's last item -- the
-                    // slots no CTA uses for this strip are zeroed, so the normaliser can sum all
-                    // a.groups slots of every strip
+                if (a.items && pd.last && active && xok && pi.ue - pi.ub < a.nch_full) {
+                    // persistent schedule, end of an item that covered less than a whole pass: its
+                    // slot's rows it never visited are zeroed (the normaliser sums every slot the
+                    // strip's items wrote, over all rows)
                     const int nf = a.nch_full;
                     const int total = pi.ue - pi.ub, c0 = pi.ub % nf;
-                    const int zero_from = a.items[pi.it].w >> 16;
-                    auto zero_rows = [&](int z, int c) {
-                        float *zp = a.pz + ((long long)z * (C::D + 1) + plane) * plane_out + x;
+                    float *zp = a.pz + ((long long)pd.slot * (C::D + 1) + plane) * plane_out + x;
+                    for (int c = 0; c < nf; ++c) {
+                        if ((c - c0 + nf) % nf < total) continue;
                         for (int o = 0; o < OR; ++o) {
                             const int row = pd.ty0 + c * C::KB + H0 + o;
                             if (row < ty1) zp[(long long)(row - a.out_row0) * a.W] = 0.f;
                         }
-                    };
-                    for (int c = 0; c < nf; ++c) {
-                        if (total < nf && (c - c0 + nf) % nf >= total) zero_rows(pd.slot, c);
-                        if (zero_from > 0)
-                            for (int z = zero_from; z < a.groups; ++z) zero_rows(z, c);
                     }
                 }
                 gs += pass_rows<C>(pd);

@@ -36,12 +36,16 @@ __global__ void normalize_groups_kernel(const float *__restrict__ pz, int groups
                                         long long npix, const float *__restrict__ mu_dev,
                                         float mu0, float mu1, float mu2, float mu3, float mu4,
                                         float mu5, float mu6, float mu7, float *__restrict__ out,
-                                        unsigned long long *diag, float inv_m, float z_floor) {
+                                        unsigned long long *diag, float inv_m, float z_floor, int W,
+                                        const int *__restrict__ strip_slots) {
     const float mu[8] = {mu0, mu1, mu2, mu3, mu4, mu5, mu6, mu7};
     (void)mu_dev;
     const long long e = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
     const bool valid = e < npix;
     const long long gstride = (long long)(D + 1) * npix;
+    // persistent schedule: the slots written for this pixel's 32-column strip (a VEC group never
+    // straddles strips: VEC = 4 needs W % 4 == 0)
+    if (strip_slots && valid) groups = strip_slots[(int)(e % W) >> 5];
     float z[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) z[v] = 0.f;
@@ -109,11 +113,13 @@ __global__ void normalize_groups_kernel(const float *__restrict__ pz, int groups
 __global__ void finalize_partial_kernel(const float *__restrict__ pz, int groups, int D, int d,
                                         int rows, int W, float mu0, float mu1, float mu2,
                                         float mu3, float mu4, float mu5, float mu6, float mu7,
-                                        int rpb, float *__restrict__ PZ) {
+                                        int rpb, float *__restrict__ PZ,
+                                        const int *__restrict__ strip_slots) {
     const float mu[8] = {mu0, mu1, mu2, mu3, mu4, mu5, mu6, mu7};
     const long long npix = (long long)rows * W;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= npix) return;
+    if (strip_slots) groups = strip_slots[(int)(e % W) >> 5];   // persistent schedule
     const long long gstride = (long long)(D + 1) * npix;
     float z = 0.f;
     for (int g = 0; g < groups; ++g) z += pz[g * gstride + (long long)D * npix + e];
@@ -152,7 +158,7 @@ __global__ void diag_reset_kernel(unsigned long long *diag) {
 
 cudaError_t launch_normalize_groups(const float *pz, int groups, int D, int d, int rows, int W,
                                     const float *mu, float *out, float *diag, float inv_m,
-                                    float z_floor, cudaStream_t s) {
+                                    float z_floor, cudaStream_t s, const int *strip_slots) {
     const long long npix = (long long)rows * W;
     const int threads = 256;
     auto dg = reinterpret_cast<unsigned long long *>(diag);
@@ -164,22 +170,23 @@ cudaError_t launch_normalize_groups(const float *pz, int groups, int D, int d, i
         const long long n = npix / 4;
         normalize_groups_kernel<4><<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
             pz, groups, D, d, npix, nullptr, mu[0], mu[1], mu[2], mu[3], mu[4], mu[5], mu[6], mu[7],
-            out, dg, inv_m, z_floor);
+            out, dg, inv_m, z_floor, W, strip_slots);
     } else {
         normalize_groups_kernel<1><<<(unsigned)((npix + threads - 1) / threads), threads, 0, s>>>(
             pz, groups, D, d, npix, nullptr, mu[0], mu[1], mu[2], mu[3], mu[4], mu[5], mu[6], mu[7],
-            out, dg, inv_m, z_floor);
+            out, dg, inv_m, z_floor, W, strip_slots);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_finalize_partial(const float *pz, int groups, int D, int d, int rows, int W,
-                                    const float *mu, int rows_per_band, float *PZ, cudaStream_t s) {
+                                    const float *mu, int rows_per_band, float *PZ, cudaStream_t s,
+                                    const int *strip_slots) {
     const long long npix = (long long)rows * W;
     const int threads = 256;
     finalize_partial_kernel<<<(unsigned)((npix + threads - 1) / threads), threads, 0, s>>>(
         pz, groups, D, d, rows, W, mu[0], mu[1], mu[2], mu[3], mu[4], mu[5], mu[6], mu[7],
-        rows_per_band, PZ);
+        rows_per_band, PZ, strip_slots);
     return cudaGetLastError();
 }
 

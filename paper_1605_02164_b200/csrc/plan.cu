@@ -365,13 +365,20 @@ struct RealBatch {
     int groups, stride;
 };
 
-// Persistent schedule for the v6 kernel (FusedArgs::items): one CTA per SM slot, each taking an
-// equal share of the work line (strip, pass, chunk) -- a contiguous range that may start and end
-// mid-pass -- instead of whole (strip, tile, sample group) CTAs, whose count rarely divides into
-// whole waves (config 2: 128 CTAs on 148 SMs). A CTA's range splits into one item per strip it
-// touches; the items of a strip write consecutive partial slots. Used when the cost model (chunk
-// steps incl. the A/KB-chunk pipeline fill per pass) beats the classic grid by > 0.5 %.
-// Returns the slot count (groups) or 0 when the classic grid stays.
+// Persistent schedule for the v6 kernel (FusedArgs::items): one CTA per SM slot running a list of
+// items (strip, range of its (pass, chunk) work line, partial slot), instead of whole (strip,
+// tile, sample group) CTAs whose count rarely divides into whole waves (config 2: 128 CTAs on 148
+// SMs). The classic units (strip x, sample group g: a range of two-sample passes over the full
+// height) are dealt out in whole rounds -- CTA c takes units c, c + nC, ... -- so at any time the
+// CTAs sweep neighbouring strips at the same rows and share their halo columns of f in L2, as the
+// classic waves do; the units left over after the last whole round (config 5: 136 of 1024; config
+// 2: all 128) are cut into nC equal shares of their (pass, chunk) work line, on whole passes when a
+// share spans >= 50 passes (else mid-pass: a partial pass streams its own A-row halo first). A
+// unit's first piece writes slot g, further pieces extra slots >= the group count; an item that
+// covers less than a whole pass zeroes the rows it never visited and each strip's last item zeroes
+// the slots no CTA uses for it, so the normaliser sums the same slot count everywhere. Chosen when
+// the chunk-step cost model (incl. the A/KB-chunk pipeline fill per pass) of the busiest CTA beats
+// the classic grid by > 0.5 %. Returns the slot count (groups) or 0 when the classic grid stays.
 int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int groups, cudaStream_t s) {
     const KernelInfo &ki = p->kinfo;
     if (p->persistent == 0 || (ki.variant != 4 && ki.variant != 7)) return 0;
@@ -381,8 +388,10 @@ int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int gr
     const long long nf = (out_rows + ki.kb - 1) / ki.kb;
     const long long P = (ns + ki.sp - 1) / ki.sp;
     const long long nC = (long long)sm_count() * std::max(1, ki.occupancy);
-    const long long U = nx * P * nf;
-    if (U < 4 * nC) return 0;
+    if (nx * P * nf < 4 * nC) return 0;
+    const long long Gc = std::max(1LL, std::min<long long>(groups, P));
+    const long long key[5] = {nx, nf, P, nC, (ki.variant * 2 + (p->persistent == 2 ? 1 : 0)) * 65536 + Gc};
+    if (std::equal(key, key + 5, p->pers_key)) return p->pers_groups;
     const double fill = (double)((ki.kb + 2 * ki.R + 15) / 16 * 16) / ki.kb;   // A / KB chunk-times per pass
     // classic grid: whole waves of CTAs, each ceil(samples / SP) passes over its tile
     const long long ny = (out_rows + tile_rows - 1) / tile_rows;
@@ -390,36 +399,89 @@ int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int gr
     const long long waves = (ctas + nC - 1) / nC;
     const long long gpass = ((ns + groups - 1) / groups + ki.sp - 1) / ki.sp;
     const double t_classic = (double)waves * gpass * ((tile_rows + ki.kb - 1) / ki.kb + fill);
-    const double share = (double)U / nC;
-    const double t_pers = std::ceil(share) + (share / nf + 2.0) * fill;
-    // the model matches the measurements: config 2 predicted 0.91, measured 0.90 (kernel time);
-    // config 5 predicted 0.989, measured 0.989; config 3 predicted 1.003 (stays classic)
-    if (p->persistent == 1 && !(t_pers < 0.995 * t_classic)) return 0;
-    const long long key[5] = {nx, nf, P, nC, ki.variant};
-    if (std::equal(key, key + 5, p->pers_key)) return p->pers_groups;
+
+    std::vector<std::vector<int4>> mine(nC);
+    std::vector<int> nslot(nx, 0);   // slots handed out per strip, in item order
+    auto unit = [&](long long u, long long &x, long long &g, long long &pb, long long &pe) {
+        x = u % nx;
+        g = u / nx;
+        pb = P * g / Gc;
+        pe = P * (g + 1) / Gc;
+    };
+    const long long units = nx * Gc, rounds = units / nC;
+    for (long long r = 0; r < rounds; ++r)
+        for (long long c = 0; c < nC; ++c) {
+            long long x, g, pb, pe;
+            unit(r * nC + c, x, g, pb, pe);
+            if (pe > pb) mine[c].push_back(make_int4((int)x, (int)(pb * nf), (int)(pe * nf), nslot[x]++));
+        }
+    // the tail: units [rounds * nC, units), strip-major, the tail units of one strip merged into
+    // one pass range (consecutive groups are consecutive passes), as one work line of chunk steps
+    // cut into nC shares
+    std::vector<long long> tx, tpb, tpe;   // per tail range: strip, first pass, end pass
+    {
+        std::vector<long long> lo(nx, -1), hi(nx, -1);
+        for (long long u = rounds * nC; u < units; ++u) {
+            long long x, g, pb, pe;
+            unit(u, x, g, pb, pe);
+            if (lo[x] < 0 || pb < lo[x]) lo[x] = pb;
+            hi[x] = std::max(hi[x], pe);
+        }
+        for (long long x = 0; x < nx; ++x)
+            if (lo[x] >= 0 && hi[x] > lo[x]) { tx.push_back(x); tpb.push_back(lo[x]); tpe.push_back(hi[x]); }
+    }
+    std::vector<long long> start(1, 0);
+    for (size_t i = 0; i < tx.size(); ++i) start.push_back(start.back() + (tpe[i] - tpb[i]) * nf);
+    const long long TW = start.back();
+    const double tshare = (double)TW / nC;
+    const long long gran = (tshare / nf >= 50.0) ? nf : 1;
+    auto cut = [&](long long c) { return c >= nC ? TW : (TW * c / nC + gran / 2) / gran * gran; };
+    for (long long c = 0; c < nC && TW > 0; ++c) {
+        long long w0 = cut(c);
+        const long long w1 = cut(c + 1);
+        while (w0 < w1) {
+            const long long i = std::upper_bound(start.begin(), start.end(), w0) - start.begin() - 1;
+            const long long x = tx[i], pb = tpb[i];
+            const long long e = std::min(w1, start[i + 1]);
+            const long long a0 = w0 - start[i], a1 = e - start[i];
+            mine[c].push_back(make_int4((int)x, (int)(pb * nf + a0), (int)(pb * nf + a1), nslot[x]++));
+            w0 = e;
+        }
+    }
+    // busiest CTA under the cost model: chunk steps + one fill per pass an item streams
+    double t_pers = 0.0;
+    for (long long c = 0; c < nC; ++c) {
+        double tc = 0.0;
+        for (const int4 &it : mine[c]) {
+            const long long passes = (it.z - 1) / nf - it.y / nf + 1;
+            tc += (double)(it.z - it.y) + passes * fill;
+        }
+        t_pers = std::max(t_pers, tc);
+    }
+    // measured: config 2 predicted 0.91, measured 0.90 (kernel time); config 5 (whole rounds +
+    // tail) predicted 0.99; config 3 stays classic
+    if (p->persistent == 1 && !(t_pers < 0.995 * t_classic)) {
+        std::copy(key, key + 5, p->pers_key);
+        p->pers_groups = 0;
+        return 0;
+    }
     std::vector<int4> items;
     std::vector<int> off(nC + 1);
-    std::vector<int> cnt(nx, 0);
-    std::vector<int> last_item(nx, -1);
-    const long long per_strip = P * nf;
     for (long long c = 0; c < nC; ++c) {
-        long long u0 = U * c / nC;
-        const long long u1 = U * (c + 1) / nC;
         off[c] = (int)items.size();
-        while (u0 < u1) {
-            const long long x = u0 / per_strip;
-            const long long e = std::min(u1, (x + 1) * per_strip);
-            last_item[x] = (int)items.size();
-            items.push_back(make_int4((int)x, (int)(u0 - x * per_strip), (int)(e - x * per_strip), cnt[x]++));
-            u0 = e;
-        }
+        for (const int4 &it : mine[c]) items.push_back(it);
     }
     off[nC] = (int)items.size();
     int G = 1;
-    for (long long x = 0; x < nx; ++x) G = std::max(G, cnt[x]);
-    if (G > 0xFFFF) return 0;
-    for (long long x = 0; x < nx; ++x)   // the strip's last item zeroes the slots no CTA uses for it
-        if (cnt[x] < G) items[last_item[x]].w |= cnt[x] << 16;
+    for (long long x = 0; x < nx; ++x) G = std::max(G, nslot[x]);
+    if (p->dstrip_cap < (size_t)nx) {
+        cudaFree(p->dstrip_slots);
+        p->dstrip_slots = nullptr;
+        p->dstrip_cap = 0;
+        if (cudaMalloc(&p->dstrip_slots, sizeof(int) * nx) != cudaSuccess) { cudaGetLastError(); return 0; }
+        p->dstrip_cap = nx;
+        p->gen += 1;
+    }
     if (p->ditems_cap < items.size()) {
         cudaFree(p->ditems);
         p->ditems = nullptr;
@@ -439,7 +501,8 @@ int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int gr
     // ordered before the launches that read it (the copy is synchronous; it runs once per schedule)
     if (cudaStreamSynchronize(s) != cudaSuccess ||
         cudaMemcpy(p->ditems, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(p->ditem_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(p->ditem_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(p->dstrip_slots, nslot.data(), sizeof(int) * nx, cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -468,7 +531,7 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
         const long long key_nf = (out_rows + ki.kb - 1) / ki.kb;
         const long long key_P = (k1 - k0 + ki.sp - 1) / std::max(1, ki.sp);
         const bool cached = p->pers_key[1] == key_nf && p->pers_key[2] == key_P &&
-                            p->pers_key[0] == (p->W + kTX - 1) / kTX && p->pers_key[4] == ki.variant;
+                            p->pers_key[0] == (p->W + kTX - 1) / kTX && p->pers_key[4] / 65536 / 2 == ki.variant;
         // never allocate or copy while the stream is captured: only a cached schedule may be used
         if (!capturing || cached) pers = plan_persistent(p, out_rows, k1 - k0, tile_rows, groups, s);
         if (pers) {
@@ -538,6 +601,7 @@ bf_status_t run_fused(bf_vec_plan_t p, const float *f, int slab_rows, int slab_r
         grid = dim3(p->pers_ctas, 1, 1);
     }
     p->last_persistent = pers ? 1 : 0;
+    p->last_strip_slots = pers ? p->dstrip_slots : nullptr;
     p->last_tile_rows = tile_rows;
     p->last_groups = groups;
     p->last_ctas = (long long)grid.x * grid.y * grid.z;
@@ -909,7 +973,7 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
         cudaFree(p->dpz); cudaFree(p->ddiag); cudaFree(p->dU); cudaFree(p->dfpad);
         cudaFree(p->dhost_in); cudaFree(p->dhost_out); cudaFree(p->drec); cudaFree(p->drtab); cudaFree(p->drun); cudaFree(p->dmse);
         cudaFree(p->dkeys); cudaFree(p->dlab); cudaFree(p->dt_batch); cudaFree(p->dX_batch);
-        cudaFree(p->ditems); cudaFree(p->ditem_off);
+        cudaFree(p->ditems); cudaFree(p->ditem_off); cudaFree(p->dstrip_slots);
         if (p->gexec) cudaGraphExecDestroy(p->gexec);
         if (p->copy_out) cudaStreamSynchronize(p->copy_out);
         if (p->order_ev) {
@@ -982,7 +1046,8 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     if (st != BF_OK) return st;
     BF_CUDA(launch_diag_reset(p->ddiag, s));
     BF_CUDA(launch_normalize_groups(p->dpz, groups, D, p->d, row1 - row0, p->W, p->mu, out,
-                                    p->ddiag, 1.0f / p->M, (float)p->z_floor, s));
+                                    p->ddiag, 1.0f / p->M, (float)p->z_floor, s,
+                                    p->engine == 1 ? nullptr : p->last_strip_slots));
     if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)(row1 - row0) * p->W, s));
     // engine 1 per batch: staged 2 kernels (row, column), tiled 5 (3 tile passes, 2 scans)
     // engine 0: pad, fused kernel (variant 8: two launches), diagnostics reset, normalise
@@ -1193,7 +1258,8 @@ bf_status_t bf_vec_filter_partial(bf_vec_plan_t p, const float *f, int k0, int k
                                       : run_fused(p, f, p->H, 0, 0, p->H, k0, k1, s, &groups);
     if (st != BF_OK) return st;
     BF_CUDA(launch_finalize_partial(p->dpz, groups, p->engine == 1 ? p->d : p->kinfo.D, p->d, p->H, p->W, p->mu,
-                                    rows_per_band, PZ, s));
+                                    rows_per_band, PZ, s,
+                                    p->engine == 1 ? nullptr : p->last_strip_slots));
     p->last_launches = 3;
     p->last = s;
     return BF_OK;

@@ -110,7 +110,8 @@ def test_variant1_d8_parity(case):
 # span several strips, cover less than one pass, and with odd sample counts (one-sample passes).
 @pytest.mark.parametrize("case", [(131, 77, 3, 5.0, 30, 17, 9, "full"), (70, 96, 3, 16.0, 40, 7, 2, "diag"),
                                   (512, 70, 3, 2.0, 20, 9, 5, "diag"), (300, 200, 1, 3.3, 20, 6, 7, "full"),
-                                  (40, 33, 2, 8.0, 20, 5, 4, "full")])
+                                  (40, 33, 2, 8.0, 20, 5, 4, "full"),
+                                  (40, 320, 3, 1.0, 10, 1500, 6, "diag")])   # shares of >= 50 passes: whole-pass cuts
 def test_persistent_schedule_parity(case):
     cfg = _edge_cfg(case)
     f = random_image(cfg.H, cfg.W, cfg.d, seed=cfg.seed, smooth=True)
