@@ -102,10 +102,9 @@ struct VecT<2> {
 
 // Shared memory per CTA: ring of NS = TY + 1 rows x 2D planes x SW floats, then the taps.
 template <int D, int BX, int TY>
-__global__ void __launch_bounds__(16 * TY) direct_tiled_kernel(const float *__restrict__ UF, int H, int W,
-                                                                   int r, int Hp, int Wpp, int SW, int nch,
-                                                                   const __grid_constant__ DirectTArgs da,
-                                                                   float *__restrict__ out) {
+__device__ __forceinline__ void direct_tiled_body(const float *__restrict__ UF, int H, int W, int r, int Hp,
+                                                  int Wpp, int SW, int nch, const DirectTArgs &da,
+                                                  float *__restrict__ out) {
     constexpr int NP = 2 * D, NS = TY + 1, TXW = 16 * BX, kDirThreads = 16 * TY;
     extern __shared__ __align__(16) float dsm[];
     float *ring = dsm;
@@ -253,6 +252,26 @@ __global__ void __launch_bounds__(16 * TY) direct_tiled_kernel(const float *__re
     }
 }
 
+// Two entry points over one body: the 256-thread d <= 4 instances are compiled for 3 CTAs per SM
+// (80 registers, 72 B of spills outside the inner loop): +2.4 % on config 5 and +2.7 % on config 3
+// against the compiler's own choice (102 registers, 2 CTAs per SM; profiles/r02_direct_minblocks.txt);
+// the others keep the compiler's choice (an explicit minBlocks = 1 raised d = 3 to 134 registers
+// and 1 CTA per SM, and slowed d = 8 by 14 %).
+template <int D, int BX, int TY>
+__global__ void __launch_bounds__(16 * TY) direct_tiled_kernel(const float *__restrict__ UF, int H, int W, int r,
+                                                               int Hp, int Wpp, int SW, int nch,
+                                                               const __grid_constant__ DirectTArgs da,
+                                                               float *__restrict__ out) {
+    direct_tiled_body<D, BX, TY>(UF, H, W, r, Hp, Wpp, SW, nch, da, out);
+}
+template <int D, int BX, int TY>
+__global__ void __launch_bounds__(16 * TY, 3) direct_tiled_kernel_occ3(const float *__restrict__ UF, int H, int W,
+                                                                       int r, int Hp, int Wpp, int SW, int nch,
+                                                                       const __grid_constant__ DirectTArgs da,
+                                                                       float *__restrict__ out) {
+    direct_tiled_body<D, BX, TY>(UF, H, W, r, Hp, Wpp, SW, nch, da, out);
+}
+
 template <int D>
 constexpr int dir_bx() { return D <= 4 ? 4 : 2; }
 
@@ -268,11 +287,13 @@ cudaError_t launch_direct_dt(const float *UF, int H, int W, int r, int Hp, int W
     constexpr size_t smem_max = sizeof(float) * ((size_t)NS * NP * SW_max + kDirLw + 4);
     static_assert(smem_max <= 227 * 1024, "direct ring exceeds shared memory");
     if (smem > smem_max) return cudaErrorInvalidValue;
+    constexpr bool occ3 = TY == 16 && D <= 4;
+    auto kern = occ3 ? direct_tiled_kernel_occ3<D, BX, TY> : direct_tiled_kernel<D, BX, TY>;
     static std::atomic<uint64_t> attr_done{0};
-    cudaError_t e = ensure_smem_attr(direct_tiled_kernel<D, BX, TY>, smem_max, attr_done);
+    cudaError_t e = ensure_smem_attr(kern, smem_max, attr_done);
     if (e != cudaSuccess) return e;
     dim3 grid((W + 16 * BX - 1) / (16 * BX), (H + TY - 1) / TY);
-    direct_tiled_kernel<D, BX, TY><<<grid, 16 * TY, smem, s>>>(UF, H, W, r, Hp, Wpp, SW, nch, da, out);
+    kern<<<grid, 16 * TY, smem, s>>>(UF, H, W, r, Hp, Wpp, SW, nch, da, out);
     return cudaGetLastError();
 }
 
