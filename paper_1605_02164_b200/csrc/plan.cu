@@ -507,6 +507,7 @@ int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int gr
         return 0;
     }
     std::copy(key, key + 5, p->pers_key);
+    p->gen += 1;   // the tables were rewritten: a captured filter graph of another shape must re-capture
     p->pers_groups = G;
     p->pers_items = (int)items.size();
     p->pers_ctas = (int)nC;

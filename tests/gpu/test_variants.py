@@ -154,3 +154,29 @@ def test_persistent_config2_default_and_graph():
     s.synchronize()
     assert p.info("graph_ready") == 1
     assert torch.equal(out, e1)
+
+
+def test_persistent_tables_rewritten_invalidate_graph():
+    """A call of another shape rewrites the persistent item tables; a CUDA graph captured for the
+    first shape must then re-capture (plan generation), not replay against the rewritten tables."""
+    import torch
+    cfg = CONFIGS[2]
+    fg = torch.from_numpy(make_image(cfg)).cuda()
+    p = H.gpu_plan(cfg)
+    p.set_option("graph", 0)
+    ref = p.filter(fg).clone()
+    p.set_option("graph", 1)
+    s = torch.cuda.Stream()
+    out = torch.empty_like(fg)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            p.filter(fg, out)
+    s.synchronize()
+    assert p.info("graph_ready") == 1 and p.info("last_persistent") == 1
+    with torch.cuda.stream(s):
+        p.filter_partial(fg, 0, cfg.M // 2 + 7)          # another pass count: new tables
+        for _ in range(3):
+            out.zero_()
+            p.filter(fg, out)
+    s.synchronize()
+    assert torch.equal(out, ref)
