@@ -42,13 +42,16 @@ struct CfgT2 {
     static constexpr int WIN = TX + 2 * R;
     static constexpr int MS = cs_stride(WIN);
     static constexpr int A = round_up(KB + 2 * R, 16);
-    // OV (pass overlap, where TMEM holds it: 2 samples x 2 x 2A columns <= 512, i.e. R <= 24): the
-    // ring holds 2A rows, so the producers fill the next pass's first A rows while the consumers
-    // still read the last chunk of the current one (its window ends A rows before the new rows'
-    // slots); every chunk then waits only for the consumers' chunk q-2. Without OV the first chunk
-    // of a pass waits for the whole previous pass (A + KB rows).
-    static constexpr bool OV = SP * 2 * (2 * A) <= 512;
-    static constexpr int HROWS = OV ? 2 * A : A + KB;
+    // Pass overlap: the ring holds HROWS = min(2A, what TMEM holds: 512 columns / (2 SP)) >= A + KB
+    // rows. The first SPLIT = HROWS - A rows of a pass's A-row fill land in slots the previous
+    // pass's last chunk no longer reads, so the producers write them while the consumers still
+    // read that chunk (waiting only for chunk q-2, as every chunk does), and wait for the last
+    // chunk only before the rest. R <= 24: SPLIT >= A, the whole fill overlaps (OV); R = 30: 48 of
+    // 80 rows; R = 48: 16 of 112.
+    static constexpr int HCAP = 512 / (2 * SP) / 16 * 16;
+    static constexpr int HROWS = (2 * A <= HCAP) ? 2 * A : (A + KB > HCAP ? A + KB : HCAP);
+    static constexpr int SPLIT = HROWS - A;
+    static constexpr bool OV = SPLIT >= A;
     static constexpr int RING = HROWS - R + (MW_ > 0 ? 2 * SH : 0);   // modulators run <= 2 sub-steps ahead
     static constexpr int NIN = 8 + 2 * R;
     static constexpr int RCOLS = 2 * HROWS;                 // TMEM columns per ring
@@ -78,6 +81,7 @@ struct CfgT2 {
     static_assert(CW_ == 1 || CW_ == 2, "one or two consumer warps per pair");
     static_assert(MW_ == 0 || MW_ == 4, "no or four modulation warps");
     static_assert(SP * RCOLS <= 512, "two rings in TMEM");
+    static_assert(SPLIT % SH == 0 && SPLIT >= KB, "fill split on a sub-step boundary");
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(WIN <= 256, "TMA box dimension");
 };
@@ -404,15 +408,16 @@ __global__ void __launch_bounds__(C::NT, 1) mcsf_tmem2_kernel(const __grid_const
                         tk[s][c] = (c < a.d && s < np) ? __ldg(a.t + (long long)(k + s) * a.d + c) : 0.f;
                 for (int ci = 0; ci < nchunks; ++ci, ++q) {
                     const bool first_c = (ci == 0);
-                    if (first_c && !C::OV) {
-                        if (q >= 1) mbar_wait(&empty[(q - 1) & 1], ((q - 1) >> 1) & 1);
-                    } else if (q >= 2) {
-                        mbar_wait(&empty[q & 1], ((q - 2) >> 1) & 1);
-                    }
+                    if (q >= 2) mbar_wait(&empty[q & 1], ((q - 2) >> 1) & 1);   // consumers' chunk q-2 done
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const int u_begin = first_c ? 0 : C::A + (ci - 1) * C::KB;
                     const int n_new = first_c ? C::A : C::KB;
                     for (int s0 = 0; s0 < n_new; s0 += C::SH, buf ^= 1, ++it) {
+                        if (!C::OV && first_c && s0 == C::SPLIT && q >= 1) {
+                            // the rest of the fill reuses the slots of the previous pass's last chunk
+                            mbar_wait(&empty[(q - 1) & 1], ((q - 1) >> 1) & 1);
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        }
                         const int gsub = gs + u_begin + s0;
                         float2 *gb0 = gbase + (2 * buf + 0) * GSZ;
                         float2 *gb1 = gbase + (2 * buf + 1) * GSZ;

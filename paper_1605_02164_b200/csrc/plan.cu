@@ -388,7 +388,7 @@ int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int gr
     const long long nf = (out_rows + ki.kb - 1) / ki.kb;
     const long long P = (ns + ki.sp - 1) / ki.sp;
     const long long nC = (long long)sm_count() * std::max(1, ki.occupancy);
-    if (nx * P * nf < 4 * nC) return 0;
+    if (p->persistent != 2 && nx * P * nf < 4 * nC) return 0;   // forced: any size (idle CTAs get no items)
     const long long Gc = std::max(1LL, std::min<long long>(groups, P));
     const long long key[5] = {nx, nf, P, nC, (ki.variant * 2 + (p->persistent == 2 ? 1 : 0)) * 65536 + Gc};
     if (std::equal(key, key + 5, p->pers_key)) return p->pers_groups;

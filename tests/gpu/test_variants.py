@@ -121,6 +121,7 @@ def test_persistent_schedule_parity(case):
     p.set_option("persistent", 2)
     res = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)
     print(case, "persistent", p.info("last_persistent"), "groups", p.info("groups"), res)
+    assert p.info("last_persistent") == 1
     H.assert_gates(res)
     p.set_option("persistent", 0)
     res0 = H.gates(cfg, *H.gpu_run(p, f), S_o, P_o, Z_o)

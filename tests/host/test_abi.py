@@ -132,6 +132,16 @@ def test_new_entry_points_validate_arguments_without_gpu():
         assert lib.bf_vec_filter_partial_p2p(h, dummy, 0, 2, peers, 1, 0, 3, None) == -1      # slots > samples
         assert lib.bf_vec_filter_partial_p2p(h, dummy, 0, 4, peers, 1, 0, 2, None) == -6      # not sampled yet
         assert lib.bf_vec_normalize_slots(h, dummy, 0, 0, 4, dummy, None) == -1
+        # pipelined host frames: null buffers are refused; before a device is bound, BF_E_STATE
+        assert lib.bf_vec_filter_host_async(h, None, dummy, None) == -1
+        assert lib.bf_vec_filter_host_async(None, dummy, dummy, None) == -1
+        assert lib.bf_vec_filter_host_async(h, dummy, dummy, None) == -6
+        assert lib.bf_vec_host_sync(None) == -1
+        assert lib.bf_vec_host_sync(h) == -6
+        # new options: documented values accepted, others refused
+        for name, good, bad in (("persistent", 2, 3), ("direct_rows", 8, 5), ("rec_store", 1, 2)):
+            assert lib.bf_vec_set_option(h, name.encode(), float(good)) == 0
+            assert lib.bf_vec_set_option(h, name.encode(), float(bad)) == -1
     finally:
         lib.bf_vec_plan_destroy(h)
 
