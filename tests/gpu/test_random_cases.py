@@ -69,3 +69,46 @@ def test_random_case(case):
     print(case, res)
     assert res["gate_a_z"] <= H.GATE_A and res["gate_a_p"] <= H.GATE_A, res
     assert res["gate_b_z01"] <= H.GATE_B, res
+
+
+def _persistent_cases(n=16):
+    """Random shapes for the persistent schedule of the v6 kernel (forced): shares that start and end
+    mid-pass, span strips, leave CTAs idle, odd sample counts; d <= 3, Gaussian or box taps."""
+    rng = np.random.default_rng(2027)
+    out = []
+    for i in range(n):
+        d = int(rng.choice([1, 2, 3, 3]))
+        Hh = int(rng.integers(8, 200))
+        W = int(rng.integers(8, 260))
+        s = float(rng.choice([1.0, 2.0, 3.3, 5.0, 8.0, 10.0]))
+        M = int(rng.integers(1, 41))
+        spatial = str(rng.choice(["gaussian", "gaussian", "box"]))
+        out.append((i, Hh, W, d, s, M, spatial))
+    return out
+
+
+@pytest.mark.parametrize("case", _persistent_cases(), ids=lambda c: f"pcase{c[0]}")
+def test_random_persistent_case(case):
+    i, Hh, W, d, s, M, spatial = case
+    rng = np.random.default_rng(500 + i)
+    C = np.diag(rng.uniform(20.0, 60.0, d) ** 2)
+    cfg = small_config(d=d, H=Hh, W=W, sigma_s=s, N=20, M=M, seed=300 + i, C=C)
+    f = random_image(Hh, W, d, seed=i, smooth=bool(i % 2))
+    Q, a = oplan.diagonalize(C)
+    Y = draws.y_draws(cfg.seed, M, d, 20)
+    S_o, P_o, Z_o = native.mcsf_full(f, Q, a, 20, Y, s, spatial=spatial)
+    from paper_1605_02164_b200 import Plan
+    p = Plan(Hh, W, d, s, C, 20, M, cfg.seed)
+    p.set_option("spatial_kernel", oplan.SPATIAL_KINDS[spatial])
+    p.set_option("persistent", 2)
+    p.sample_freqs()
+    S_g, P_g, Z_g = H.gpu_run(p, f)
+    if p.info("variant") in (4, 7):
+        assert p.info("last_persistent") == 1
+    res = H.gates(cfg, S_g, P_g, Z_g, S_o, P_o, Z_o)
+    ok = Z_o / M >= 0.1
+    res["gate_b_z01"] = float(np.abs(S_g - S_o)[..., ok].max()) if ok.any() else 0.0
+    print(case, p.info("variant"), p.info("groups"), res)
+    assert res["gate_a_z"] <= H.GATE_A and res["gate_a_p"] <= H.GATE_A, res
+    assert res["gate_b_z01"] <= H.GATE_B, res
+    p.close()
