@@ -365,43 +365,14 @@ struct RealBatch {
     int groups, stride;
 };
 
-// Persistent schedule for the v6 kernel (FusedArgs::items): one CTA per SM slot running a list of
-// items (strip, range of its (pass, chunk) work line, partial slot), instead of whole (strip,
-// tile, sample group) CTAs whose count rarely divides into whole waves (config 2: 128 CTAs on 148
-// SMs). The classic units (strip x, sample group g: a range of two-sample passes over the full
-// height) are dealt out in whole rounds -- CTA c takes units c, c + nC, ... -- so at any time the
-// CTAs sweep neighbouring strips at the same rows and share their halo columns of f in L2, as the
-// classic waves do; the units left over after the last whole round (config 5: 136 of 1024; config
-// 2: all 128) are cut into nC equal shares of their (pass, chunk) work line, on whole passes when a
-// share spans >= 50 passes (else mid-pass: a partial pass streams its own A-row halo first). A
-// unit's first piece writes slot g, further pieces extra slots >= the group count; an item that
-// covers less than a whole pass zeroes the rows it never visited and each strip's last item zeroes
-// the slots no CTA uses for it, so the normaliser sums the same slot count everywhere. Chosen when
-// the chunk-step cost model (incl. the A/KB-chunk pipeline fill per pass) of the busiest CTA beats
-// the classic grid by > 0.5 %. Returns the slot count (groups) or 0 when the classic grid stays.
-int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int groups, cudaStream_t s) {
-    const KernelInfo &ki = p->kinfo;
-    if (p->persistent == 0 || (ki.variant != 4 && ki.variant != 7)) return 0;
-    // a forced (tile_rows, groups) schedule is honoured unless persistent = 2 forces this one
-    if (p->persistent == 1 && (p->force_groups > 0 || p->force_tile_rows > 0)) return 0;
-    const long long nx = (p->W + kTX - 1) / kTX;
-    const long long nf = (out_rows + ki.kb - 1) / ki.kb;
-    const long long P = (ns + ki.sp - 1) / ki.sp;
-    const long long nC = (long long)sm_count() * std::max(1, ki.occupancy);
-    if (p->persistent != 2 && nx * P * nf < 4 * nC) return 0;   // forced: any size (idle CTAs get no items)
-    const long long Gc = std::max(1LL, std::min<long long>(groups, P));
-    const long long key[5] = {nx, nf, P, nC, (ki.variant * 2 + (p->persistent == 2 ? 1 : 0)) * 65536 + Gc};
-    if (std::equal(key, key + 5, p->pers_key)) return p->pers_groups;
-    const double fill = (double)((ki.kb + 2 * ki.R + 15) / 16 * 16) / ki.kb;   // A / KB chunk-times per pass
-    // classic grid: whole waves of CTAs, each ceil(samples / SP) passes over its tile
-    const long long ny = (out_rows + tile_rows - 1) / tile_rows;
-    const long long ctas = nx * ny * groups;
-    const long long waves = (ctas + nC - 1) / nC;
-    const long long gpass = ((ns + groups - 1) / groups + ki.sp - 1) / ki.sp;
-    const double t_classic = (double)waves * gpass * ((tile_rows + ki.kb - 1) / ki.kb + fill);
-
-    std::vector<std::vector<int4>> mine(nC);
-    std::vector<int> nslot(nx, 0);   // slots handed out per strip, in item order
+// The items of the persistent schedule (see plan_persistent): per CTA its items (strip, u_begin,
+// u_end, slot) over the strip's work line u = pass * nf + chunk, and per strip the number of slots
+// handed out. Returns the busiest CTA's cost under the chunk-step model. Host-only and pure (the
+// CPU tests check its coverage and slot invariants through bfvec_test_persistent_items).
+double persistent_items(long long nx, long long nf, long long P, long long nC, long long Gc, double fill,
+                        std::vector<std::vector<int4>> &mine, std::vector<int> &nslot) {
+    mine.assign(nC, {});
+    nslot.assign(nx, 0);   // slots handed out per strip, in item order
     auto unit = [&](long long u, long long &x, long long &g, long long &pb, long long &pe) {
         x = u % nx;
         g = u / nx;
@@ -458,6 +429,47 @@ int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int gr
         }
         t_pers = std::max(t_pers, tc);
     }
+    return t_pers;
+}
+
+// Persistent schedule for the v6 kernel (FusedArgs::items): one CTA per SM slot running a list of
+// items (strip, range of its (pass, chunk) work line, partial slot), instead of whole (strip,
+// tile, sample group) CTAs whose count rarely divides into whole waves (config 2: 128 CTAs on 148
+// SMs). The classic units (strip x, sample group g: a range of two-sample passes over the full
+// height) are dealt out in whole rounds -- CTA c takes units c, c + nC, ... -- so at any time the
+// CTAs sweep neighbouring strips at the same rows and share their halo columns of f in L2, as the
+// classic waves do; the units left over after the last whole round (config 5: 136 of 1024; config
+// 2: all 128) are cut into nC equal shares of their (pass, chunk) work line, on whole passes when a
+// share spans >= 50 passes (else mid-pass: a partial pass streams its own A-row halo first). A
+// unit's first piece writes slot g, further pieces extra slots >= the group count; an item that
+// covers less than a whole pass zeroes the rows it never visited and each strip's last item zeroes
+// the slots no CTA uses for it, so the normaliser sums the same slot count everywhere. Chosen when
+// the chunk-step cost model (incl. the A/KB-chunk pipeline fill per pass) of the busiest CTA beats
+// the classic grid by > 0.5 %. Returns the slot count (groups) or 0 when the classic grid stays.
+int plan_persistent(bf_vec_plan_t p, int out_rows, int ns, int tile_rows, int groups, cudaStream_t s) {
+    const KernelInfo &ki = p->kinfo;
+    if (p->persistent == 0 || (ki.variant != 4 && ki.variant != 7)) return 0;
+    // a forced (tile_rows, groups) schedule is honoured unless persistent = 2 forces this one
+    if (p->persistent == 1 && (p->force_groups > 0 || p->force_tile_rows > 0)) return 0;
+    const long long nx = (p->W + kTX - 1) / kTX;
+    const long long nf = (out_rows + ki.kb - 1) / ki.kb;
+    const long long P = (ns + ki.sp - 1) / ki.sp;
+    const long long nC = (long long)sm_count() * std::max(1, ki.occupancy);
+    if (p->persistent != 2 && nx * P * nf < 4 * nC) return 0;   // forced: any size (idle CTAs get no items)
+    const long long Gc = std::max(1LL, std::min<long long>(groups, P));
+    const long long key[5] = {nx, nf, P, nC, (ki.variant * 2 + (p->persistent == 2 ? 1 : 0)) * 65536 + Gc};
+    if (std::equal(key, key + 5, p->pers_key)) return p->pers_groups;
+    const double fill = (double)((ki.kb + 2 * ki.R + 15) / 16 * 16) / ki.kb;   // A / KB chunk-times per pass
+    // classic grid: whole waves of CTAs, each ceil(samples / SP) passes over its tile
+    const long long ny = (out_rows + tile_rows - 1) / tile_rows;
+    const long long ctas = nx * ny * groups;
+    const long long waves = (ctas + nC - 1) / nC;
+    const long long gpass = ((ns + groups - 1) / groups + ki.sp - 1) / ki.sp;
+    const double t_classic = (double)waves * gpass * ((tile_rows + ki.kb - 1) / ki.kb + fill);
+
+    std::vector<std::vector<int4>> mine;
+    std::vector<int> nslot;
+    const double t_pers = persistent_items(nx, nf, P, nC, Gc, fill, mine, nslot);
     // measured: config 2 predicted 0.91, measured 0.90 (kernel time); config 5 (whole rounds +
     // tail) predicted 0.99; config 3 stays classic
     if (p->persistent == 1 && !(t_pers < 0.995 * t_classic)) {
@@ -1652,3 +1664,31 @@ bf_status_t bf_vec_philox4x64_10(const uint64_t ctr[4], const uint64_t key[2], u
 }
 
 }  // extern "C"
+
+// Test hook (not part of include/bfvec.h): the persistent schedule's item table for a given shape,
+// so the CPU tests can check that every strip's work line is covered exactly once and its slots are
+// distinct (tests/host/test_persistent_items.py). items: 4 ints per item; off: nC + 1 ints; nslot:
+// nx ints. Returns the item count, or -1 if `cap` items do not fit.
+extern "C" int bfvec_test_persistent_items(int nx, int nf, int P, int nC, int Gc, double fill, int *items, int cap,
+                                           int *off, int *nslot, double *t_pers) {
+    if (nx < 1 || nf < 1 || P < 1 || nC < 1 || Gc < 1 || Gc > P) return -1;
+    std::vector<std::vector<int4>> mine;
+    std::vector<int> ns;
+    const double t = persistent_items(nx, nf, P, nC, Gc, fill, mine, ns);
+    int n = 0;
+    for (int c = 0; c < nC; ++c) {
+        off[c] = n;
+        for (const int4 &it : mine[c]) {
+            if (n >= cap) return -1;
+            items[4 * n + 0] = it.x;
+            items[4 * n + 1] = it.y;
+            items[4 * n + 2] = it.z;
+            items[4 * n + 3] = it.w;
+            ++n;
+        }
+    }
+    off[nC] = n;
+    for (int x = 0; x < nx; ++x) nslot[x] = ns[x];
+    if (t_pers) *t_pers = t;
+    return n;
+}
