@@ -153,6 +153,8 @@ struct RecTArgs {
     float *rbg;           // (ns, 2(d+1), H, W) row-blurred planes written by pass 1 and read by pass 2
                           // (option "rec_store" = 1), or null: pass 2 recomputes the row blur
     RecTabs th, tv;
+    float4 zpc[kRecT];    // (z_0^m, z_1^m), m < kRecT, in the parameter space: full tiles' summaries take
+                          // them as uniform constant operands (no per-element shared-memory loads)
 };
 cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s);
 

@@ -827,6 +827,14 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     a.rbg = p->rec_store ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
     rec_axis(p->sigma_s, p->W, &a.row);
     rec_axis(p->sigma_s, p->H, &a.col);
+    {   // the pole powers z_j^m, m < kRecT (as in ensure_rec_tabs), as kernel parameters
+        const double bj[2] = {1.783, 1.723}, wj[2] = {0.6318, 1.997};
+        for (int m = 0; m < kRecT; ++m) {
+            const Cplx z0 = cexp_(-bj[0] * m / p->sigma_s, wj[0] * m / p->sigma_s);
+            const Cplx z1 = cexp_(-bj[1] * m / p->sigma_s, wj[1] * m / p->sigma_s);
+            a.zpc[m] = make_float4((float)z0.r, (float)z0.i, (float)z1.r, (float)z1.i);
+        }
+    }
     int slot = -1;
     if (p->profile) {
         if (p->ev_count == bf_vec_plan_s::kEvRing) collect_profile(p);
