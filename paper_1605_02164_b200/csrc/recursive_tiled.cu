@@ -288,6 +288,10 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
     const bool rb_load = MODE == 2 && a.rbg != nullptr;   // pass 2 reads pass 1's row blur
     if (MODE >= 1 && !rb_load && s0 < s1 && lane < Ly)
         get_states(a.Eh, a.Bh, a.UVh, a.th, s0, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
+    // the column states are loaded a whole sample ahead too (round 2: issued at the row stage, the
+    // consumer of their loads was the top stall site of pass 2; pass 2 21.95 -> 21.77 ms)
+    if (MODE == 2 && s0 < s1 && lane < Lx)
+        get_states(a.Ev, a.Bv, a.UVv, a.tv, s0, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
     for (int b = s0; b < s1; ++b) {
         const int k = a.k0 + b;
         float tk[D];
@@ -307,7 +311,6 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
 
         // ---- row stage: lane = row ----
         const bool full = Lx == T && Ly == T;
-        if (MODE == 2 && lane < Lx) get_states(a.Ev, a.Bv, a.UVv, a.tv, b, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
         if (lane < Ly) {
             const float2 *hrow = cs + lane * TP;
             const float *frow = fs + ((p > 0 ? p - 1 : 0) * T + lane) * TP;
@@ -371,6 +374,8 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
             } else {
                 if (full) blur_accumulate<true>(a.col, T, c0, c1, cs + lane, cl, cr, acc);
                 else blur_accumulate<false>(a.col, Ly, c0, c1, cs + lane, cl, cr, acc);
+                if (MODE == 2 && b + 1 < s1)
+                    get_states(a.Ev, a.Bv, a.UVv, a.tv, b + 1, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
             }
         }
     }
