@@ -138,7 +138,8 @@ bf_status_t bf_vec_filter_host(bf_vec_plan_t plan, const float *f_host, float *o
  * (on the device) for the frame that used it two calls earlier.
  *   f_host, out_host  host (d, H, W) fp32; pinned (cudaHostAlloc / torch pin_memory) for the copies
  *                     to be asynchronous. The caller must keep f_host unchanged and out_host alive
- *                     until bf_vec_host_sync returns (or alternate host buffers per frame).
+ *                     until bf_vec_host_sync returns (or alternate host buffers per frame);
+ *                     f_host and out_host must not be the same buffer (BF_E_ARG).
  * Errors: BF_E_STATE before bf_vec_sample_freqs; BF_E_CUDA.
  */
 bf_status_t bf_vec_filter_host_async(bf_vec_plan_t plan, const float *f_host, float *out_host, void *stream);

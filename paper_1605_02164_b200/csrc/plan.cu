@@ -1206,7 +1206,8 @@ bf_status_t bf_vec_filter_host(bf_vec_plan_t p, const float *f_host, float *out_
 bf_status_t bf_vec_filter_host_async(bf_vec_plan_t p, const float *f_host, float *out_host, void *stream) {
     Nvtx nvtx_("bfvec:filter_host_async");
     StreamOrder order_(valid_plan(p) ? p : nullptr, S(stream));
-    if (!valid_plan(p) || !f_host || !out_host) return BF_E_ARG;
+    // f_host == out_host would let this frame's D2H race the next frames' H2D reads
+    if (!valid_plan(p) || !f_host || !out_host || f_host == out_host) return BF_E_ARG;
     if (p->device < 0 || !p->sampled) return BF_E_STATE;
     const size_t bytes = sizeof(float) * (size_t)p->d * p->H * p->W;
     if (!p->copy_in) {

@@ -135,7 +135,8 @@ def test_new_entry_points_validate_arguments_without_gpu():
         # pipelined host frames: null buffers are refused; before a device is bound, BF_E_STATE
         assert lib.bf_vec_filter_host_async(h, None, dummy, None) == -1
         assert lib.bf_vec_filter_host_async(None, dummy, dummy, None) == -1
-        assert lib.bf_vec_filter_host_async(h, dummy, dummy, None) == -6
+        assert lib.bf_vec_filter_host_async(h, dummy, dummy, None) == -1     # in == out
+        assert lib.bf_vec_filter_host_async(h, dummy, ctypes.c_void_p(32), None) == -6
         assert lib.bf_vec_host_sync(None) == -1
         assert lib.bf_vec_host_sync(h) == -6
         # new options: documented values accepted, others refused
