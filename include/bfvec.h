@@ -108,6 +108,9 @@ bf_status_t bf_vec_get_draws(bf_vec_plan_t plan, int32_t *X, float *t, double *Q
  * (Alg. 1). f, out: device planar (d, H, W) float32; out may not
  * alias f. Returns BF_OK or BF_W_ALIAS (data leaves the raised cosine's main
  * lobe; output still written). BF_W_SMALL_Z is reported by bf_vec_diag.
+ * BF_E_UNSUPPORTED when the FIR engine has no kernel for (d, r): r = ceil(3 sigma_s) > 64, or
+ * 5 <= d <= 8 with r > 24 (the nine (cos, sin) pairs' rings exceed shared memory / TMEM there);
+ * the recursive engine (option "engine" = 1) covers every (d, sigma_s).
  */
 bf_status_t bf_vec_filter(bf_vec_plan_t plan, const float *f, float *out, void *stream);
 
