@@ -149,12 +149,17 @@ struct RecTArgs {
     RecAxis row, col;
     float2 *Eh, *Bh;      // (ns, 2(d+1), 2, ntx, H): row tiles' causal end / anticausal start states
     float2 *Ev, *Bv;      // (ns, 2(d+1), 2, nty, W): the same for the column tiles
-    float4 *UVh, *UVv;    // (ns, 2(d+1), 2, H) / (.., W): line states (u_{-1}, v_n)
+    float4 *UVh, *UVv;    // (ns, 2(d+1), 2, nlh) / (.., W): line states (u_{-1}, v_n)
+    int nlh;              // lines of the row arrays: H (rec_impl 1), H + 8 nty (rec_impl 2: + virtual lines)
+    float *vl;            // rec_impl 2: (ns, 2(d+1), nty, 8, W) virtual-line values (column summaries
+                          // of the modulated planes, real / imaginary parts), or null (rec_impl 1)
     float *rbg;           // (ns, 2(d+1), H, W) row-blurred planes written by pass 1 and read by pass 2
                           // (option "rec_store" = 1), or null: pass 2 recomputes the row blur
     RecTabs th, tv;
     float4 zpc[kRecT];    // (z_0^m, z_1^m), m < kRecT, in the parameter space: full tiles' summaries take
                           // them as uniform constant operands (no per-element shared-memory loads)
+    float4 zpq[kRecT];    // the same regrouped (Re z_0^m, Re z_1^m, Im z_0^m, Im z_1^m): both poles of one
+                          // real line in one FFMA2 (rec_impl 2's virtual-line summaries)
 };
 cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s);
 

@@ -765,11 +765,15 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     const int ntx = (p->W + kRecT - 1) / kRecT, nty = (p->H + kRecT - 1) / kRecT;
     const long long tiles = (long long)ntx * nty;
     const size_t px = (size_t)p->H * p->W;
-    // per sample in flight: row / column summaries (E, B) and line states
-    const size_t sum_h = (size_t)NQ * 2 * ntx * p->H, sum_v = (size_t)NQ * 2 * nty * p->W;
-    const size_t uv_h = (size_t)NQ * 2 * p->H, uv_v = (size_t)NQ * 2 * p->W;
-    const size_t rb_per = p->rec_store ? sizeof(float) * (size_t)NQ * px : 0;   // stored row blur
-    const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v) + rb_per;
+    // rec_impl 2: the row arrays also hold 8 virtual lines per tile row
+    const bool vlines = p->rec_impl == 2;
+    const int nlh = p->H + (vlines ? 8 * nty : 0);
+    // per sample in flight: row / column summaries (E, B) and line states (+ virtual-line values)
+    const size_t sum_h = (size_t)NQ * 2 * ntx * nlh, sum_v = (size_t)NQ * 2 * nty * p->W;
+    const size_t uv_h = (size_t)NQ * 2 * nlh, uv_v = (size_t)NQ * 2 * p->W;
+    const size_t rb_per = (p->rec_store && !vlines) ? sizeof(float) * (size_t)NQ * px : 0;   // stored row blur
+    const size_t vl_per = vlines ? sizeof(float) * (size_t)NQ * nty * 8 * p->W : 0;
+    const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v) + rb_per + vl_per;
     int nb = 1, g = 1;
     bf_status_t st = BF_OK;
     for (int attempt = 0; attempt < 2; ++attempt) {
@@ -824,7 +828,9 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     a.Bv = a.Ev + (size_t)nb * sum_v;
     a.UVh = reinterpret_cast<float4 *>(a.Bv + (size_t)nb * sum_v);
     a.UVv = a.UVh + (size_t)nb * uv_h;
-    a.rbg = p->rec_store ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
+    a.rbg = rb_per ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
+    a.nlh = nlh;
+    a.vl = vlines ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
     rec_axis(p->sigma_s, p->W, &a.row);
     rec_axis(p->sigma_s, p->H, &a.col);
     {   // the pole powers z_j^m, m < kRecT (as in ensure_rec_tabs), as kernel parameters
@@ -833,6 +839,7 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
             const Cplx z0 = cexp_(-bj[0] * m / p->sigma_s, wj[0] * m / p->sigma_s);
             const Cplx z1 = cexp_(-bj[1] * m / p->sigma_s, wj[1] * m / p->sigma_s);
             a.zpc[m] = make_float4((float)z0.r, (float)z0.i, (float)z1.r, (float)z1.i);
+            a.zpq[m] = make_float4((float)z0.r, (float)z1.r, (float)z0.i, (float)z1.i);
         }
     }
     int slot = -1;
@@ -864,7 +871,7 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
 
 // samples [k0, k1) of the recursive engine into p->dpz (groups = samples per batch)
 bf_status_t run_recursive(bf_vec_plan_t p, const float *f, int k0, int k1, cudaStream_t s, int *groups_out) {
-    if (p->rec_impl == 1) return run_recursive_tiled(p, f, k0, k1, s, groups_out);
+    if (p->rec_impl >= 1) return run_recursive_tiled(p, f, k0, k1, s, groups_out);
     const int ns = k1 - k0;
     const size_t px = (size_t)p->H * p->W;
     // per sample in flight: y1 + y2 (2 x 2(d+1) planes) + one partial group ((d+1) planes)
@@ -1072,7 +1079,7 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)(row1 - row0) * p->W, s));
     // engine 1 per batch: staged 2 kernels (row, column), tiled 5 (3 tile passes, 2 scans)
     // engine 0: pad, fused kernel (variant 8: two launches), diagnostics reset, normalise
-    p->last_launches = ((p->engine == 1) ? 2 + (p->rec_impl == 1 ? 5 : 2) * ((p->M + p->last_batch - 1) / p->last_batch)
+    p->last_launches = ((p->engine == 1) ? 2 + (p->rec_impl >= 1 ? 5 : 2) * ((p->M + p->last_batch - 1) / p->last_batch)
                                          : 4 + (p->kinfo.variant == 8 ? 1 : 0)) + (p->lab ? 2 : 0);
     p->last = s;
     return p->alias ? BF_W_ALIAS : BF_OK;
@@ -1612,7 +1619,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         return BF_OK;
     }
     if (!std::strcmp(name, "rec_impl")) {
-        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
         p->rec_impl = (int)v;
         return BF_OK;
     }

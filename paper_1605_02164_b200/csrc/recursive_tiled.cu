@@ -119,8 +119,9 @@ struct TileSmem {
     static constexpr int OFF_CS = D * T * TP;                 // floats; fs[D][T][TP] first
     static constexpr int OFF_RB = OFF_CS + 2 * T * TP;        // cs: [T][TP] float2
     static constexpr int OFF_ZP = OFF_RB + (MODE >= 1 ? NQ * T * TP : 0);   // zp[2 axes][T] float4
-    static constexpr int OFF_ACC = OFF_ZP + 2 * 4 * T;                     // MODE 2: acc[NP][T][T]
-    static constexpr size_t BYTES = sizeof(float) * (size_t)(OFF_ACC + (MODE == 2 ? NP * T * T : 0));
+    static constexpr int OFF_ACC = OFF_ZP + 2 * 4 * T;   // MODE 2: acc[NP][T][T]; MODE 0: vs[NP][2][8][TP]
+    static constexpr size_t BYTES =
+        sizeof(float) * (size_t)(OFF_ACC + (MODE == 2 ? NP * T * T : MODE == 0 ? NP * 16 * TP : 0));
 };
 
 // zero-started summaries of one pair over a segment of n <= T elements,
@@ -167,6 +168,30 @@ __device__ __forceinline__ void summaries_full(const float4 (&zt)[T], X xat, St 
         e.ui[0] = fma2s(pe.y, x, e.ui[0]);
         e.ur[1] = fma2s(pe.z, x, e.ur[1]);
         e.ui[1] = fma2s(pe.w, x, e.ui[1]);
+    }
+}
+
+// rec_impl 2: index of a virtual-line value (s, q, ty, v, x); v = (k * 2 + kind) * 2 + part for the
+// column pole k, kind 0 = e / 1 = b, part 0 = real / 1 = imaginary
+__device__ __forceinline__ long long vlidx(int s, int q, int ty, int v, int x, int NQ, int nty, int W) {
+    return ((((long long)s * NQ + q) * nty + ty) * 8 + v) * W + x;
+}
+
+// summaries of ONE real line over a segment of n <= T elements, both poles in one FFMA2:
+// pr/pi = (Re / Im z_0^m, Re / Im z_1^m); e*, b* hold (pole 0, pole 1)
+template <bool FULL, class X, class Z>
+__device__ __forceinline__ void summaries_line(int n, X xat, Z zat, float2 &er, float2 &ei, float2 &br, float2 &bi) {
+    er = ei = br = bi = f2(0.f, 0.f);
+#pragma unroll
+    for (int m = 0; m < T; ++m) {
+        if (FULL || m < n) {
+            const float x = xat(m);
+            const float4 pb = zat(m), pe = zat((FULL ? T : n) - 1 - m);
+            br = fma2s(x, f2(pb.x, pb.y), br);
+            bi = fma2s(x, f2(pb.z, pb.w), bi);
+            er = fma2s(x, f2(pe.x, pe.y), er);
+            ei = fma2s(x, f2(pe.z, pe.w), ei);
+        }
     }
 }
 
@@ -245,6 +270,62 @@ __device__ __forceinline__ void blur_accumulate(const RecAxis &ax, int n, const 
     }
 }
 
+// rec_impl 2, pass 0, one warp = pair p: the column summaries of the pair's modulated planes over the
+// tile (lane = column) are the tile's segment of the 8 virtual lines per plane,
+//   C_{k,e}[x] = sum_m w_k^{Ly-1-m} X[y0+m, x],  C_{k,b}[x] = sum_m w_k^m X[y0+m, x]   (real, imag parts);
+// the row blur is linear, so rowblur(C)[x] is the column summary of the row-blurred plane that pass 1
+// of rec_impl 1 computed from a full row blur of the tile. The values go to a.vl (read by the
+// virtual-line kernel) and, through shared memory vs[h][v][TP], into the row summaries of the virtual
+// lines (lane = (h, v), both poles per FFMA2), stored as rows H + 8 ty + v of Eh / Bh.
+template <int NP, class XIN>
+__device__ __forceinline__ void virtual_lines(const RecTArgs &a, float *vs, const float4 *zp, XIN xin, int b, int p,
+                                              int tx, int ty, int lane, int Lx, int Ly, bool full) {
+    constexpr int NQ = 2 * NP;
+    if (lane < Lx) {
+        auto xat = [&](int m) -> float2 { return xin(m, lane); };
+        St ce, cb;
+        if (full) summaries_full(a.zpc, xat, ce, cb);
+        else summaries<false>(zp + T, Ly, xat, ce, cb);
+        const int x = tx * T + lane;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int kind = 0; kind < 2; ++kind) {
+                const St &sv = kind ? cb : ce;
+                const int v = (k * 2 + kind) * 2;
+                const float val[2][2] = {{sv.ur[k].x, sv.ui[k].x}, {sv.ur[k].y, sv.ui[k].y}};
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int part = 0; part < 2; ++part) {
+                        vs[(h * 8 + v + part) * TP + lane] = val[h][part];
+                        a.vl[vlidx(b, 2 * p + h, ty, v + part, x, NQ, a.nty, a.W)] = val[h][part];
+                    }
+            }
+    }
+    __syncwarp();
+    if (lane < 16) {
+        const int h = lane >> 3, v = lane & 7;
+        const float *row = vs + (h * 8 + v) * TP;
+        float2 er, ei, br, bi;
+        auto xat = [&](int m) -> float { return row[m]; };
+        if (Lx == T) {
+            summaries_line<true>(T, xat, [&](int m) -> float4 { return a.zpq[m]; }, er, ei, br, bi);
+        } else {
+            summaries_line<false>(Lx, xat, [&](int m) -> float4 {
+                const float4 z = zp[m];
+                return make_float4(z.x, z.z, z.y, z.w);
+            }, er, ei, br, bi);
+        }
+        const int q = 2 * p + h, line = a.H + ty * 8 + v;
+        a.Eh[sidx(b, q, 0, tx, line, NQ, a.ntx, a.nlh)] = f2(er.x, ei.x);
+        a.Eh[sidx(b, q, 1, tx, line, NQ, a.ntx, a.nlh)] = f2(er.y, ei.y);
+        a.Bh[sidx(b, q, 0, tx, line, NQ, a.ntx, a.nlh)] = f2(br.x, bi.x);
+        a.Bh[sidx(b, q, 1, tx, line, NQ, a.ntx, a.nlh)] = f2(br.y, bi.y);
+    }
+    __syncwarp();   // vs is rewritten for the next sample
+}
+
 template <int NP, int MODE>
 __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(const __grid_constant__ RecTArgs a) {
     using L = TileSmem<NP, MODE>;
@@ -287,7 +368,7 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
     St rl, rr, cl, cr;
     const bool rb_load = MODE == 2 && a.rbg != nullptr;   // pass 2 reads pass 1's row blur
     if (MODE >= 1 && !rb_load && s0 < s1 && lane < Ly)
-        get_states(a.Eh, a.Bh, a.UVh, a.th, s0, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
+        get_states(a.Eh, a.Bh, a.UVh, a.th, s0, p, tx, y0 + lane, NQ, a.ntx, a.nlh, rl, rr);
     // the column states are loaded a whole sample ahead too (round 2: issued at the row stage, the
     // consumer of their loads was the top stall site of pass 2; pass 2 21.95 -> 21.77 ms)
     if (MODE == 2 && s0 < s1 && lane < Lx)
@@ -325,15 +406,19 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
                 St e, bb;
                 if (full) summaries_full(a.zpc, xat, e, bb);
                 else summaries<false>(zp, Lx, xat, e, bb);
-                put_state(a.Eh, e, b, p, tx, y, NQ, a.ntx, H);
-                put_state(a.Bh, bb, b, p, tx, y, NQ, a.ntx, H);
+                put_state(a.Eh, e, b, p, tx, y, NQ, a.ntx, a.nlh);
+                put_state(a.Bh, bb, b, p, tx, y, NQ, a.ntx, a.nlh);
             } else if (!rb_load) {
                 float *r0 = rb + (2 * p * T + lane) * TP, *r1 = rb + ((2 * p + 1) * T + lane) * TP;
                 if (full) blur_segment<true>(a.row, T, xat, rl, rr, r0, r1);
                 else blur_segment<false>(a.row, Lx, xat, rl, rr, r0, r1);
             }
         }
-        if (MODE == 0) continue;
+        if (MODE == 0) {
+            if (a.vl != nullptr) virtual_lines<NP>(a, sm + L::OFF_ACC + p * 16 * TP, zp, xin, b, p, tx, ty, lane,
+                                                   Lx, Ly, full);
+            continue;
+        }
         if (rb_load && lane < Lx) {
             // pass 1's exact row blur of this tile (planes 2p, 2p+1): lane = column, coalesced rows
             const float *g0 = a.rbg + (((long long)b * NQ + 2 * p) * H + y0) * W + x0 + lane;
@@ -346,7 +431,7 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
             }
         }
         if (!rb_load && b + 1 < s1 && lane < Ly)
-            get_states(a.Eh, a.Bh, a.UVh, a.th, b + 1, p, tx, y0 + lane, NQ, a.ntx, H, rl, rr);
+            get_states(a.Eh, a.Bh, a.UVh, a.th, b + 1, p, tx, y0 + lane, NQ, a.ntx, a.nlh, rl, rr);
         // the column stage of pair p reads only rb planes 2p, 2p+1 (written by this warp) and cs
         // (complete since the barrier after the modulation): a warp barrier suffices
         __syncwarp();
@@ -450,6 +535,61 @@ __global__ void __launch_bounds__(256) rect_scan_kernel(float2 *__restrict__ E, 
     UV[sqj * nlines + line] = make_float4(um1.x, um1.y, vn.x, vn.y);
 }
 
+// rec_impl 2, pass 1: the exact row blur of the virtual lines over their tile segments from their
+// entering states (rows H + 8 ty + v of the row scan) -- by linearity the column summaries of the
+// row-blurred planes, written to Ev / Bv for the column scan. One warp per (tile row, 4 tiles, pair):
+// lane = (tile i of the 4, virtual line v), both planes of the pair per FFMA2; the 4 tiles' segments
+// are staged through shared memory so every global access is coalesced.
+template <int NP>
+__global__ void __launch_bounds__(32) rect_vline_kernel(const __grid_constant__ RecTArgs a) {
+    constexpr int NQ = 2 * NP;
+    __shared__ float vb[16 * 4 * TP];   // inputs [h][v][i][TP]
+    __shared__ float ob[16 * 4 * TP];   // row-blurred [h][v][i][TP]
+    const int lane = threadIdx.x, i = lane >> 3, v = lane & 7;
+    const int nq4 = (a.ntx + 3) / 4;
+    const int quad = blockIdx.x % nq4, ty = blockIdx.x / nq4, p = blockIdx.y, g = blockIdx.z;
+    const int G = a.g1;
+    const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
+    const int tx = quad * 4 + i, xq = quad * 4 * T;
+    const int Lx = (tx < a.ntx) ? min(T, a.W - tx * T) : 0;
+    const int ncols = min(4 * T, a.W - xq);
+    const int line = a.H + ty * 8 + v;
+    St L, R;
+    for (int b = s0; b < s1; ++b) {
+        if (Lx > 0) get_states(a.Eh, a.Bh, a.UVh, a.th, b, p, tx, line, NQ, a.ntx, a.nlh, L, R);
+#pragma unroll
+        for (int hv = 0; hv < 16; ++hv) {
+            const float *src = a.vl + vlidx(b, 2 * p + (hv >> 3), ty, hv & 7, xq, NQ, a.nty, a.W);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (u * T + lane < ncols) vb[(hv * 4 + u) * TP + lane] = __ldg(src + u * T + lane);
+        }
+        __syncwarp();
+        if (Lx > 0) {
+            const float *x0p = vb + (v * 4 + i) * TP, *x1p = vb + ((8 + v) * 4 + i) * TP;
+            auto xat = [&](int m) -> float2 { return f2(x0p[m], x1p[m]); };
+            float *r0 = ob + (v * 4 + i) * TP, *r1 = ob + ((8 + v) * 4 + i) * TP;
+            if (Lx == T) blur_segment<true>(a.row, T, xat, L, R, r0, r1);
+            else blur_segment<false>(a.row, Lx, xat, L, R, r0, r1);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int kind = 0; kind < 2; ++kind) {
+                    const int vr = h * 8 + (k * 2 + kind) * 2;
+                    float2 *dst = (kind ? a.Bv : a.Ev) + sidx(b, 2 * p + h, k, ty, xq, NQ, a.nty, a.W);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (u * T + lane < ncols)
+                            dst[u * T + lane] = f2(ob[(vr * 4 + u) * TP + lane], ob[((vr + 1) * 4 + u) * TP + lane]);
+                }
+        __syncwarp();   // vb / ob are rewritten for the next sample
+    }
+}
+
 template <int NP, int MODE>
 cudaError_t launch_tile(const RecTArgs &a, int groups, cudaStream_t s) {
     const size_t smem = TileSmem<NP, MODE>::BYTES;
@@ -471,8 +611,15 @@ template <int NP>
 cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
     const long long nq = (long long)a.ns * 2 * NP;
     cudaError_t e = launch_tile<NP, 0>(a, a.g1, s);
-    if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.H, nq, s);
-    if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
+    if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.nlh, nq, s);
+    if (e == cudaSuccess) {
+        if (a.vl != nullptr) {
+            rect_vline_kernel<NP><<<dim3(((a.ntx + 3) / 4) * a.nty, NP, a.g1), 32, 0, s>>>(a);
+            e = cudaGetLastError();
+        } else {
+            e = launch_tile<NP, 1>(a, a.g1, s);
+        }
+    }
     if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
     if (e == cudaSuccess) e = launch_tile<NP, 2>(a, a.g3, s);
     return e;

@@ -17,7 +17,7 @@ from workloads.configs import random_image
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("rec_impl", [1, 0])
+@pytest.mark.parametrize("rec_impl", [2, 1, 0])
 @pytest.mark.parametrize("sigma_s", [2.0, 5.0, 10.0])
 def test_recursive_blur_within_half_intensity_of_fir(sigma_s, rec_impl):
     from paper_1605_02164_b200 import Plan
@@ -55,7 +55,7 @@ def _median_ms(p, f, out, reps=9):
     return float(np.median(ts))
 
 
-@pytest.mark.parametrize("rec_impl", [1, 0])
+@pytest.mark.parametrize("rec_impl", [2, 1, 0])
 def test_recursive_runtime_independent_of_sigma(rec_impl):
     from paper_1605_02164_b200 import Plan
     H = W = 512

@@ -20,7 +20,7 @@ pytestmark = pytest.mark.gpu
 _IMPL = {"rec_impl": 1}
 
 
-@pytest.fixture(autouse=True, params=[1, 0], ids=["tiled", "staged"])
+@pytest.fixture(autouse=True, params=[2, 1, 0], ids=["vlines", "tiled", "staged"])
 def rec_impl(request):
     """Every test runs on both implementations of the engine (option "rec_impl")."""
     _IMPL["rec_impl"] = request.param
