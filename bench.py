@@ -51,7 +51,7 @@ def parse(argv=None):
     ap.add_argument("--variant", type=int, default=0, help="fused-kernel variant (0 = library default)")
     ap.add_argument("--engine", type=int, default=0, help="0 truncated FIR (default), 1 recursive O(1) engine")
     ap.add_argument("--sigma", type=float, default=0.0, help="override the config's sigma_s (engine sweeps)")
-    ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled (default)")
+    ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled, 2 tiled + virtual lines (default)")
     ap.add_argument("--persistent", type=int, default=-1,
                     help="v6 kernel schedule: 1 auto (library default), 0 classic grid, 2 persistent")
     ap.add_argument("--rec-store", type=int, default=-1,
@@ -476,8 +476,9 @@ def run_ours(args, cfg):
     achieved = flops / (fused_ms / 1e3) / 1e12
     kname = KERNEL_NAMES.get(plan.info("variant"), "mcsf_fused_kernel")
     if args.engine == 1:
-        kname = ("rect_tile_kernel x3 + rect_scan_kernel x2" if plan.info("rec_impl") == 1
-                 else "rec_row_kernel+rec_col_kernel")
+        kname = {1: "rect_tile_kernel x3 + rect_scan_kernel x2",
+                 2: "rect_tile_kernel x2 + rect_vline_kernel + rect_scan_kernel x2"}.get(
+                     plan.info("rec_impl"), "rec_row_kernel+rec_col_kernel")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": measured_traffic(cfg, kname, units_per_launch,
                                         {"tile_rows": plan.info("tile_rows"), "groups": plan.info("groups"),

@@ -316,12 +316,16 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 samples (each stratum [j/M, (j+1)/M) used once, random order; DESIGN.md
  *                 reading R17; the paper's "improving the Monte Carlo integration",
  *                 PAPER.md:313). Same estimator Eq. (14); X still B(N, 1/2)-distributed.
- *   "rec_impl"    engine 1: 1 (default) tiled -- 32 x 32 tiles, the exact states entering
- *                 each tile from per-tile summaries and a scan along every line, the blurred
- *                 planes stay in shared memory; 0 staged -- a row pass and a
- *                 column pass through HBM scratch. Same arithmetic, results equal to fp32
- *                 rounding (both gated against the oracle).
- *   "rec_store"   engine 1, tiled: 1 pass 1 stores its exact row blur (2(d+1) fp32 planes per
+ *   "rec_impl"    engine 1: 2 (default) tiled with virtual lines -- 32 x 32 tiles, the exact
+ *                 states entering each tile from per-tile summaries and a scan along every
+ *                 line; the column summaries of the row-blurred planes come from the row blur
+ *                 of 8 "virtual lines" per tile row (the column summaries of the modulated
+ *                 planes; linearity), so only pass 2 blurs whole tiles, and the blurred planes
+ *                 stay in shared memory; 1 tiled -- as 2 but pass 1 row-blurs
+ *                 every tile to form the column summaries; 0 staged -- a row pass and a column
+ *                 pass through HBM scratch. Same arithmetic, results equal to fp32 rounding
+ *                 (all three gated against the oracle).
+ *   "rec_store"   engine 1, rec_impl 1 (ignored by 2): 1 pass 1 stores its exact row blur (2(d+1) fp32 planes per
  *                 sample in flight) and pass 2 reads it instead of recomputing it; 0 (default)
  *                 recompute (measured 2 % faster on config 5)
  *   "rec_batch"   engine 1: samples per batch (0 = auto: at most 256 and 40 % of the free

@@ -221,7 +221,7 @@ struct bf_vec_plan_s {
     int engine = 0;            // 0 truncated FIR (Eq. (1) window), 1 recursive Deriche (reading R16)
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
     float *drec = nullptr;     // recursive engine scratch (y1, y2; tiled: summaries)
-    int rec_impl = 1;          // recursive engine: 0 staged (row / column passes via HBM), 1 tiled
+    int rec_impl = 2;          // recursive engine: 0 staged (row / column passes via HBM), 1 tiled, 2 tiled + virtual lines
     float2 *drtab = nullptr;   // tiled recursive engine: pole-power tables of both axes
     size_t drtab_n = 0;
     int sampler = 0;           // 0 iid binomial draws (reading R9), 1 stratified (reading R17)
