@@ -477,7 +477,7 @@ def run_ours(args, cfg):
     kname = KERNEL_NAMES.get(plan.info("variant"), "mcsf_fused_kernel")
     if args.engine == 1:
         kname = {1: "rect_tile_kernel x3 + rect_scan_kernel x2",
-                 2: "rect_tile_kernel x2 + rect_vline_kernel + rect_scan_kernel x2"}.get(
+                 2: "rect_tile_kernel x2 + rect_scan_kernel + rect_vscan_kernel"}.get(
                      plan.info("rec_impl"), "rec_row_kernel+rec_col_kernel")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": measured_traffic(cfg, kname, units_per_launch,

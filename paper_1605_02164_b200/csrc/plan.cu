@@ -1077,9 +1077,11 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
                                     p->ddiag, 1.0f / p->M, (float)p->z_floor, s,
                                     p->engine == 1 ? nullptr : p->last_strip_slots));
     if (p->lab) BF_CUDA(launch_lab_to_srgb(out, out, (long long)(row1 - row0) * p->W, s));
-    // engine 1 per batch: staged 2 kernels (row, column), tiled 5 (3 tile passes, 2 scans)
+    // engine 1 per batch: staged 2 kernels (row, column), tiled 5 (3 tile passes, 2 scans), tiled with
+    // virtual lines 4 (2 tile passes, 2 scans)
     // engine 0: pad, fused kernel (variant 8: two launches), diagnostics reset, normalise
-    p->last_launches = ((p->engine == 1) ? 2 + (p->rec_impl >= 1 ? 5 : 2) * ((p->M + p->last_batch - 1) / p->last_batch)
+    p->last_launches = ((p->engine == 1) ? 2 + (p->rec_impl == 2 ? 4 : p->rec_impl == 1 ? 5 : 2) *
+                                                   ((p->M + p->last_batch - 1) / p->last_batch)
                                          : 4 + (p->kinfo.variant == 8 ? 1 : 0)) + (p->lab ? 2 : 0);
     p->last = s;
     return p->alias ? BF_W_ALIAS : BF_OK;

@@ -16,6 +16,11 @@
 //   scan rows      : zero-started row states per tile + (u_{-1}, v_n) per row
 //   pass 1 (tile)  : exact row blur of the tile into shared memory, column summaries
 //   scan columns   : the same along columns
+// rec_impl 2 (default) drops pass 1: the column summaries of the row-blurred planes are, by linearity,
+// the row blur of the column summaries of the modulated planes -- 8 "virtual lines" per tile row
+// (pole, kind, real / imaginary part), formed in pass 0 and appended to the row lines of the row
+// scan; the column scan (rect_vscan_kernel) row-blurs their tile segments from their entering states
+// and scans the result, so only pass 2 blurs whole tiles.
 //   pass 2 (tile)  : exact row blur, exact column blur, Re[conj(H) blur] (Alg. 1) summed
 //                    over the group's samples in a shared-memory accumulator, one partial plane
 //                    set per group.
@@ -88,26 +93,42 @@ __device__ __forceinline__ void put_state(float2 *A, const St &s, int b, int p, 
         A[sidx(b, 2 * p + 1, j, t, line, NQ, nt, nlines)] = f2(s.ur[j].y, s.ui[j].y);
     }
 }
-// the exact states entering tile t of a line from the scanned zero-started ones:
-// L = Lz + z^{x0} u_{-1},  R = Rz + z^{n - x0 - L} v_n
-__device__ __forceinline__ void get_states(const float2 *E, const float2 *B, const float4 *UV, const RecTabs &tb,
-                                           int b, int p, int t, int line, int NQ, int nt, int nlines, St &L,
-                                           St &R) {
+// The exact states entering tile t of a line from the scanned zero-started ones:
+//   L = Lz + z^{x0} u_{-1},  R = Rz + z^{n - x0 - L} v_n.
+// load_raw issues the loads a whole sample before their use; the arithmetic that turns them into
+// entering states runs only at the use (make_states), so no instruction waits on the loads in
+// between (round 2: the cmul / cadd right after the loads were the top long-scoreboard stall sites
+// of pass 2)
+struct RawSt {
+    float2 e[2][2], b[2][2];   // [pole j][plane h]
+    float4 uv[2][2];
+};
+__device__ __forceinline__ void load_raw(const float2 *E, const float2 *B, const float4 *UV, int b, int p, int t,
+                                         int line, int NQ, int nt, int nlines, RawSt &r) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const float2 pf = tb.pf[j * nt + t], pb = tb.pb[j * nt + t];
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int q = 2 * p + h;
-            const float2 e = E[sidx(b, q, j, t, line, NQ, nt, nlines)];
-            const float2 bb = B[sidx(b, q, j, t, line, NQ, nt, nlines)];
-            const float4 uv = UV[uidx(b, q, j, line, NQ, nlines)];
-            const float2 l = cadd(e, cmul(pf, f2(uv.x, uv.y)));
-            const float2 r = cadd(bb, cmul(pb, f2(uv.z, uv.w)));
+            r.e[j][h] = __ldg(E + sidx(b, q, j, t, line, NQ, nt, nlines));
+            r.b[j][h] = __ldg(B + sidx(b, q, j, t, line, NQ, nt, nlines));
+            r.uv[j][h] = __ldg(UV + uidx(b, q, j, line, NQ, nlines));
+        }
+}
+// pfb[j] = (z_j^{x0}, z_j^{n - x0 - L}) of this tile (shared memory)
+__device__ __forceinline__ void make_states(const RawSt &r, const float4 *pfb, St &L, St &R) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const float4 pp = pfb[j];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float4 uv = r.uv[j][h];
+            const float2 l = cadd(r.e[j][h], cmul(f2(pp.x, pp.y), f2(uv.x, uv.y)));
+            const float2 rr = cadd(r.b[j][h], cmul(f2(pp.z, pp.w), f2(uv.z, uv.w)));
             if (h == 0) {
-                L.ur[j].x = l.x; L.ui[j].x = l.y; R.ur[j].x = r.x; R.ui[j].x = r.y;
+                L.ur[j].x = l.x; L.ui[j].x = l.y; R.ur[j].x = rr.x; R.ui[j].x = rr.y;
             } else {
-                L.ur[j].y = l.x; L.ui[j].y = l.y; R.ur[j].y = r.x; R.ui[j].y = r.y;
+                L.ur[j].y = l.x; L.ui[j].y = l.y; R.ur[j].y = rr.x; R.ui[j].y = rr.y;
             }
         }
     }
@@ -119,7 +140,8 @@ struct TileSmem {
     static constexpr int OFF_CS = D * T * TP;                 // floats; fs[D][T][TP] first
     static constexpr int OFF_RB = OFF_CS + 2 * T * TP;        // cs: [T][TP] float2
     static constexpr int OFF_ZP = OFF_RB + (MODE >= 1 ? NQ * T * TP : 0);   // zp[2 axes][T] float4
-    static constexpr int OFF_ACC = OFF_ZP + 2 * 4 * T;   // MODE 2: acc[NP][T][T]; MODE 0: vs[NP][2][8][TP]
+    static constexpr int OFF_PFB = OFF_ZP + 2 * 4 * T;   // pfb[2 axes][2 poles] float4 (make_states)
+    static constexpr int OFF_ACC = OFF_PFB + 16;        // MODE 2: acc[NP][T][T]; MODE 0: vs[NP][2][8][TP]
     static constexpr size_t BYTES =
         sizeof(float) * (size_t)(OFF_ACC + (MODE == 2 ? NP * T * T : MODE == 0 ? NP * 16 * TP : 0));
 };
@@ -275,7 +297,7 @@ __device__ __forceinline__ void blur_accumulate(const RecAxis &ax, int n, const 
 //   C_{k,e}[x] = sum_m w_k^{Ly-1-m} X[y0+m, x],  C_{k,b}[x] = sum_m w_k^m X[y0+m, x]   (real, imag parts);
 // the row blur is linear, so rowblur(C)[x] is the column summary of the row-blurred plane that pass 1
 // of rec_impl 1 computed from a full row blur of the tile. The values go to a.vl (read by the
-// virtual-line kernel) and, through shared memory vs[h][v][TP], into the row summaries of the virtual
+// column scan, rect_vscan_kernel) and, through shared memory vs[h][v][TP], into the row summaries of the virtual
 // lines (lane = (h, v), both poles per FFMA2), stored as rows H + 8 ty + v of Eh / Bh.
 template <int NP, class XIN>
 __device__ __forceinline__ void virtual_lines(const RecTArgs &a, float *vs, const float4 *zp, XIN xin, int b, int p,
@@ -326,8 +348,24 @@ __device__ __forceinline__ void virtual_lines(const RecTArgs &a, float *vs, cons
     __syncwarp();   // vs is rewritten for the next sample
 }
 
+// minimum CTAs per SM: what shared memory allows (d >= 7 fits one CTA of pass 1 / 2 per SM)
+#ifndef BFVEC_REC_P2CTAS
+#define BFVEC_REC_P2CTAS 3   // pass 2 is limited to 3 CTAs per SM by its 72 KB of shared memory anyway (A/B: 21.9 -> 21.2 ms)
+#endif
 template <int NP, int MODE>
-__global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(const __grid_constant__ RecTArgs a) {
+constexpr int tile_min_ctas() {
+    return NP <= 4 ? (MODE == 2 ? BFVEC_REC_P2CTAS : 4) : (MODE == 0 || NP <= 7) ? 2 : 1;
+}
+// A/B: BFVEC_REC_EAGER turns the raw entering-state loads into states right at the load (as before
+// round 2's change) instead of at the use
+#ifdef BFVEC_REC_EAGER
+constexpr bool kEager = true;
+#else
+constexpr bool kEager = false;
+#endif
+
+template <int NP, int MODE>
+__global__ void __launch_bounds__(32 * NP, tile_min_ctas<NP, MODE>()) rect_tile_kernel(const __grid_constant__ RecTArgs a) {
     using L = TileSmem<NP, MODE>;
     constexpr int D = L::D, NQ = L::NQ;
     extern __shared__ float sm[];
@@ -346,6 +384,14 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
 
     float4 *zp = reinterpret_cast<float4 *>(sm + L::OFF_ZP);   // [0][m]: row axis, [1][m]: column axis
     if (tid < 2 * T) zp[tid] = (tid < T) ? a.th.zp[tid] : a.tv.zp[tid - T];
+    float4 *pfb = reinterpret_cast<float4 *>(sm + L::OFF_PFB);   // [0][j]: row axis (tile tx), [1][j]: column (ty)
+    if (tid < 4) {
+        const int ax = tid >> 1, j = tid & 1;
+        const RecTabs &tb = ax ? a.tv : a.th;
+        const int t = ax ? ty : tx, nt = ax ? a.nty : a.ntx;
+        const float2 pf = tb.pf[j * nt + t], pb = tb.pb[j * nt + t];
+        pfb[tid] = make_float4(pf.x, pf.y, pb.x, pb.y);
+    }
     for (int e = tid; e < D * T * T; e += 32 * NP) {   // centred f tile (reading R12), zeros outside
         const int c = e / (T * T), i = (e / T) % T, j = e % T;
         fs[(c * T + i) * TP + j] =
@@ -363,21 +409,34 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
         return f2(h.x * fv, h.y * fv);
     };
 
-    // entering states, software-pipelined: the row states of sample b are loaded during sample
-    // b-1's column stage, the column states of sample b during its row stage
+    // entering states, software-pipelined: the raw loads of sample b + 1's row (column) states are
+    // issued right after sample b's row (column) stage and turned into states at their use
+    RawSt rraw, craw;
     St rl, rr, cl, cr;
     const bool rb_load = MODE == 2 && a.rbg != nullptr;   // pass 2 reads pass 1's row blur
-    if (MODE >= 1 && !rb_load && s0 < s1 && lane < Ly)
-        get_states(a.Eh, a.Bh, a.UVh, a.th, s0, p, tx, y0 + lane, NQ, a.ntx, a.nlh, rl, rr);
-    // the column states are loaded a whole sample ahead too (round 2: issued at the row stage, the
-    // consumer of their loads was the top stall site of pass 2; pass 2 21.95 -> 21.77 ms)
-    if (MODE == 2 && s0 < s1 && lane < Lx)
-        get_states(a.Ev, a.Bv, a.UVv, a.tv, s0, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
+    __syncthreads();   // pfb
+    if (MODE >= 1 && !rb_load && s0 < s1 && lane < Ly) {
+        load_raw(a.Eh, a.Bh, a.UVh, s0, p, tx, y0 + lane, NQ, a.ntx, a.nlh, rraw);
+        if (kEager) make_states(rraw, pfb, rl, rr);
+    }
+    if (MODE == 2 && s0 < s1 && lane < Lx) {
+        load_raw(a.Ev, a.Bv, a.UVv, s0, p, ty, x0 + lane, NQ, a.nty, W, craw);
+        if (kEager) make_states(craw, pfb + 2, cl, cr);
+    }
+    // the frequencies of the next sample are loaded a sample ahead too
+    float tn[D];
+    if (s0 < s1) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + s0) * D + c);
+    }
     for (int b = s0; b < s1; ++b) {
-        const int k = a.k0 + b;
         float tk[D];
 #pragma unroll
-        for (int c = 0; c < D; ++c) tk[c] = a.t[(long long)k * D + c];
+        for (int c = 0; c < D; ++c) tk[c] = tn[c];
+        if (b + 1 < s1) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + b + 1) * D + c);
+        }
         __syncthreads();   // the previous sample's stages are done with cs / rb (and fs is complete)
         for (int e = tid; e < T * T; e += 32 * NP) {
             const int i = e / T, j = e % T;
@@ -409,6 +468,7 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
                 put_state(a.Eh, e, b, p, tx, y, NQ, a.ntx, a.nlh);
                 put_state(a.Bh, bb, b, p, tx, y, NQ, a.ntx, a.nlh);
             } else if (!rb_load) {
+                if (!kEager) make_states(rraw, pfb, rl, rr);
                 float *r0 = rb + (2 * p * T + lane) * TP, *r1 = rb + ((2 * p + 1) * T + lane) * TP;
                 if (full) blur_segment<true>(a.row, T, xat, rl, rr, r0, r1);
                 else blur_segment<false>(a.row, Lx, xat, rl, rr, r0, r1);
@@ -430,8 +490,10 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
                 r1[m * TP] = __ldg(g1 + (long long)m * W);
             }
         }
-        if (!rb_load && b + 1 < s1 && lane < Ly)
-            get_states(a.Eh, a.Bh, a.UVh, a.th, b + 1, p, tx, y0 + lane, NQ, a.ntx, a.nlh, rl, rr);
+        if (!rb_load && b + 1 < s1 && lane < Ly) {
+            load_raw(a.Eh, a.Bh, a.UVh, b + 1, p, tx, y0 + lane, NQ, a.ntx, a.nlh, rraw);
+            if (kEager) make_states(rraw, pfb, rl, rr);
+        }
         // the column stage of pair p reads only rb planes 2p, 2p+1 (written by this warp) and cs
         // (complete since the barrier after the modulation): a warp barrier suffices
         __syncwarp();
@@ -457,10 +519,13 @@ __global__ void __launch_bounds__(32 * NP, (NP <= 4) ? 4 : 2) rect_tile_kernel(c
                 put_state(a.Ev, e, b, p, ty, x, NQ, a.nty, W);
                 put_state(a.Bv, bb, b, p, ty, x, NQ, a.nty, W);
             } else {
+                if (!kEager) make_states(craw, pfb + 2, cl, cr);
                 if (full) blur_accumulate<true>(a.col, T, c0, c1, cs + lane, cl, cr, acc);
                 else blur_accumulate<false>(a.col, Ly, c0, c1, cs + lane, cl, cr, acc);
-                if (MODE == 2 && b + 1 < s1)
-                    get_states(a.Ev, a.Bv, a.UVv, a.tv, b + 1, p, ty, x0 + lane, NQ, a.nty, W, cl, cr);
+                if (MODE == 2 && b + 1 < s1) {
+                    load_raw(a.Ev, a.Bv, a.UVv, b + 1, p, ty, x0 + lane, NQ, a.nty, W, craw);
+                    if (kEager) make_states(craw, pfb + 2, cl, cr);
+                }
             }
         }
     }
@@ -535,59 +600,249 @@ __global__ void __launch_bounds__(256) rect_scan_kernel(float2 *__restrict__ E, 
     UV[sqj * nlines + line] = make_float4(um1.x, um1.y, vn.x, vn.y);
 }
 
-// rec_impl 2, pass 1: the exact row blur of the virtual lines over their tile segments from their
-// entering states (rows H + 8 ty + v of the row scan) -- by linearity the column summaries of the
-// row-blurred planes, written to Ev / Bv for the column scan. One warp per (tile row, 4 tiles, pair):
-// lane = (tile i of the 4, virtual line v), both planes of the pair per FFMA2; the 4 tiles' segments
-// are staged through shared memory so every global access is coalesced.
-template <int NP>
-__global__ void __launch_bounds__(32) rect_vline_kernel(const __grid_constant__ RecTArgs a) {
-    constexpr int NQ = 2 * NP;
-    __shared__ float vb[16 * 4 * TP];   // inputs [h][v][i][TP]
-    __shared__ float ob[16 * 4 * TP];   // row-blurred [h][v][i][TP]
-    const int lane = threadIdx.x, i = lane >> 3, v = lane & 7;
-    const int nq4 = (a.ntx + 3) / 4;
-    const int quad = blockIdx.x % nq4, ty = blockIdx.x / nq4, p = blockIdx.y, g = blockIdx.z;
-    const int G = a.g1;
-    const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
-    const int tx = quad * 4 + i, xq = quad * 4 * T;
-    const int Lx = (tx < a.ntx) ? min(T, a.W - tx * T) : 0;
-    const int ncols = min(4 * T, a.W - xq);
-    const int line = a.H + ty * 8 + v;
-    St L, R;
-    for (int b = s0; b < s1; ++b) {
-        if (Lx > 0) get_states(a.Eh, a.Bh, a.UVh, a.th, b, p, tx, line, NQ, a.ntx, a.nlh, L, R);
-#pragma unroll
-        for (int hv = 0; hv < 16; ++hv) {
-            const float *src = a.vl + vlidx(b, 2 * p + (hv >> 3), ty, hv & 7, xq, NQ, a.nty, a.W);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (u * T + lane < ncols) vb[(hv * 4 + u) * TP + lane] = __ldg(src + u * T + lane);
+// rec_impl 2: the column scan with the virtual lines' row blur folded in. Each warp owns the 32
+// columns of one tile column tx for one (sample, plane, column pole k) and one direction (kind e:
+// causal scan, kind b: anticausal). Per batch of kVS tile rows: (1) the warp stages the segments of
+// the two virtual lines it needs (real and imaginary part of the kind's column summaries) through
+// shared memory, coalesced; (2) lane (u, part) row-blurs one segment exactly from the virtual line's
+// entering states (row scan), both row poles in one float2 -- by linearity the value is the column
+// summary of the row-blurred plane; (3) lane = column, the scan over the batch as in rect_scan_kernel.
+// The column summaries never go through HBM (a separate virtual-line kernel writing them for the
+// column scan to read and rewrite, round 2's first version, moved 16 B per pixel-sample more:
+// 4.4 + 2.7 ms vs 6.6 ms per 16 config-5 samples).
+constexpr int kVS = 16;
+struct St1 {   // one real line, both poles: (pole 0, pole 1)
+    float2 ur, ui;
+};
+
+// exact blur of one real line over a segment of n elements from its entering states (l = u[x0-1],
+// r = v[x0+n]): y[m] = sum_j Re[A_j (u_j[m] + v_j[m])] - g0 x[m]; full segments interleave the two
+// directions as blur_segment does
+template <bool FULL>
+__device__ __forceinline__ void blur_line(const RecAxis &ax, int n, const float *x, const St1 &l, const St1 &r,
+                                          float *y) {
+    const float2 zr = f2(ax.zr[0], ax.zr[1]), nzi = f2(-ax.zi[0], -ax.zi[1]), zi = f2(ax.zi[0], ax.zi[1]);
+    const float2 ar = f2(ax.ar[0], ax.ar[1]), nai = f2(-ax.ai[0], -ax.ai[1]);
+    const float g0 = ax.g0;
+    auto step = [&](St1 &st, float xv) {
+        const float2 ur = st.ur;
+        st.ur = __ffma2_rn(zr, ur, __ffma2_rn(nzi, st.ui, f2(xv, xv)));
+        st.ui = __ffma2_rn(zr, st.ui, __fmul2_rn(zi, ur));
+    };
+    auto out = [&](const St1 &st) {
+        const float2 t = __ffma2_rn(ar, st.ur, __fmul2_rn(nai, st.ui));
+        return t.x + t.y;
+    };
+    St1 sf = l, sb = r;
+    if constexpr (FULL) {
+#pragma unroll 4
+        for (int i = 0; i < T / 2; ++i) {
+            const int mb = T - 1 - i;
+            const float xf = x[i], xb = x[mb];
+            step(sf, xf);
+            step(sb, xb);
+            y[i] = fmaf(-g0, xf, out(sf));
+            y[mb] = out(sb);
         }
-        __syncwarp();
-        if (Lx > 0) {
-            const float *x0p = vb + (v * 4 + i) * TP, *x1p = vb + ((8 + v) * 4 + i) * TP;
-            auto xat = [&](int m) -> float2 { return f2(x0p[m], x1p[m]); };
-            float *r0 = ob + (v * 4 + i) * TP, *r1 = ob + ((8 + v) * 4 + i) * TP;
-            if (Lx == T) blur_segment<true>(a.row, T, xat, L, R, r0, r1);
-            else blur_segment<false>(a.row, Lx, xat, L, R, r0, r1);
+#pragma unroll 4
+        for (int i = T / 2; i < T; ++i) {
+            const int mb = T - 1 - i;
+            const float xf = x[i], xb = x[mb];
+            step(sf, xf);
+            step(sb, xb);
+            y[i] += fmaf(-g0, xf, out(sf));
+            y[mb] += out(sb);
         }
-        __syncwarp();
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-#pragma unroll
-                for (int kind = 0; kind < 2; ++kind) {
-                    const int vr = h * 8 + (k * 2 + kind) * 2;
-                    float2 *dst = (kind ? a.Bv : a.Ev) + sidx(b, 2 * p + h, k, ty, xq, NQ, a.nty, a.W);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (u * T + lane < ncols)
-                            dst[u * T + lane] = f2(ob[(vr * 4 + u) * TP + lane], ob[((vr + 1) * 4 + u) * TP + lane]);
-                }
-        __syncwarp();   // vb / ob are rewritten for the next sample
+    } else {
+        for (int m = 0; m < n; ++m) {
+            step(sf, x[m]);
+            y[m] = fmaf(-g0, x[m], out(sf));
+        }
+        for (int m = n - 1; m >= 0; --m) {
+            step(sb, x[m]);
+            y[m] += out(sb);
+        }
     }
+}
+
+// the same for a full segment with the two directions packed in one float2 (causal at m = i,
+// anticausal at m = T-1-i): St's pair of values is (forward, backward), so step / re_a serve as in
+// blur_segment and no horizontal add is needed
+__device__ __forceinline__ void blur_line_full(const RecAxis &ax, const float *x, const St1 &l, const St1 &r,
+                                               float *y) {
+    St st;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        st.ur[j] = f2(j ? l.ur.y : l.ur.x, j ? r.ur.y : r.ur.x);
+        st.ui[j] = f2(j ? l.ui.y : l.ui.x, j ? r.ui.y : r.ui.x);
+    }
+    const float g0 = ax.g0;
+#pragma unroll 4
+    for (int i = 0; i < T / 2; ++i) {
+        const int mb = T - 1 - i;
+        const float2 xv = f2(x[i], x[mb]);
+        step(ax, st, xv);
+        const float2 yv = re_a(ax, st);
+        y[i] = fmaf(-g0, xv.x, yv.x);
+        y[mb] = yv.y;
+    }
+#pragma unroll 4
+    for (int i = T / 2; i < T; ++i) {
+        const int mb = T - 1 - i;
+        const float2 xv = f2(x[i], x[mb]);
+        step(ax, st, xv);
+        const float2 yv = re_a(ax, st);
+        y[i] += fmaf(-g0, xv.x, yv.x);
+        y[mb] += yv.y;
+    }
+}
+
+struct VScanSmem {
+    static constexpr int WARPS = 8, ROWS = 2 * kVS;
+    // per warp: two input buffers (the next batch streams in while the current one is processed), one output
+    static constexpr size_t BYTES = sizeof(float) * 3 * WARPS * ROWS * TP + sizeof(float2) * 2 * 128;
+};
+
+// loads of one batch that do not depend on the scan: the virtual-line segments (cp.async into vbuf),
+// this lane's line's entering-state inputs and its tile's column pole power
+struct VBatch {
+    float2 e[2], bb[2], z;
+    float4 uv[2];
+};
+
+__global__ void __launch_bounds__(256, 2) rect_vscan_kernel(const __grid_constant__ RecTArgs a, int NQ,
+                                                            long long nsqk) {
+    extern __shared__ float smv[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int WB = VScanSmem::ROWS * TP;   // floats per buffer
+    float *vbuf = smv + warp * 2 * WB;                                     // inputs [2][u][part][m]
+    float *ob = smv + (2 * VScanSmem::WARPS + warp) * WB;                  // row-blurred [u][part][m]
+    float2 *fin = reinterpret_cast<float2 *>(smv + 3 * VScanSmem::WARPS * WB);   // [2][128]
+    const int dir = threadIdx.x >> 7;
+    const int ntx = a.ntx, nty = a.nty, W = a.W;
+    const long long id = (long long)blockIdx.x * 128 + (threadIdx.x & 127);
+    const long long per = (long long)ntx * 32;
+    const long long sqk = id / per;
+    const int tx = (int)((id % per) >> 5);
+    const int x0 = tx * T, x = x0 + lane;
+    const bool wlive = sqk < nsqk;   // warp-uniform
+    const bool live = wlive && x < W;
+    const int Lx = min(T, W - x0);
+    const int k = (int)(sqk & 1);
+    const long long sq = sqk >> 1;
+    const int q = (int)(sq % NQ), s = (int)(sq / NQ);
+    // this lane's blur task in a batch: tile u_me of the batch, virtual line v_me (kind = dir)
+    const int u_me = lane & 15, part = lane >> 4, v_me = (k * 2 + dir) * 2 + part;
+    float4 pfb[2];   // row-axis tile powers of tx
+    if (wlive) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float2 pf = a.th.pf[j * ntx + tx], pb = a.th.pb[j * ntx + tx];
+            pfb[j] = make_float4(pf.x, pf.y, pb.x, pb.y);
+        }
+    }
+    float2 *A = dir ? a.Bv : a.Ev;
+    const long long base = sqk * nty * (long long)W + x;   // sidx(s, q, k, t, x) = base + t * W
+    const float2 *zl = a.tv.zl + k * nty;
+    auto tile_of = [&](int i0, int u) { return dir ? nty - 1 - (i0 + u) : i0 + u; };
+    // issue the batch starting at tile i0: segments into buffer vb (one coalesced 128 B row per
+    // (tile, part), all in flight at once, zero-filled past the image edge), the rest into registers
+    auto issue = [&](int i0, float *vb, VBatch &nx) {
+        const int nb = min(kVS, nty - i0);
+        // segment (u, part) of the batch: src0 + u * ustride + part * W
+        const float *src0 = a.vl + vlidx(s, q, tile_of(i0, 0), (k * 2 + dir) * 2, min(x, W - 1), NQ, nty, W);
+        const int ustride = (dir ? -8 : 8) * W;   // within one (sample, plane): 32-bit offsets
+        const unsigned dst0 = (unsigned)__cvta_generic_to_shared(vb + lane);
+        const int bytes = lane < Lx ? 4 : 0;
+        const float *sp = src0;
+#pragma unroll
+        for (int u = 0; u < kVS; ++u) {
+            if (u < nb) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst0 + 8u * u * TP), "l"(sp),
+                             "r"(bytes)
+                             : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst0 + 4u * (2 * u + 1) * TP),
+                             "l"(sp + W), "r"(bytes)
+                             : "memory");
+            }
+            sp += ustride;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (u_me < nb) {
+            const int t = tile_of(i0, u_me);
+            const int line = a.H + t * 8 + v_me;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                nx.e[j] = __ldg(a.Eh + sidx(s, q, j, tx, line, NQ, ntx, a.nlh));
+                nx.bb[j] = __ldg(a.Bh + sidx(s, q, j, tx, line, NQ, ntx, a.nlh));
+                nx.uv[j] = __ldg(a.UVh + uidx(s, q, j, line, NQ, a.nlh));
+            }
+            nx.z = zl[t];   // lane u holds tile u's z^{L_t}
+        }
+    };
+    float2 c = f2(0.f, 0.f);
+    VBatch cur, nxt;
+    if (wlive) issue(0, vbuf, cur);
+    for (int i0 = 0, ib = 0; i0 < nty && wlive; i0 += kVS, ib ^= 1) {
+        const int nb = min(kVS, nty - i0);
+        const float *vb = vbuf + ib * WB;
+        if (i0 + kVS < nty) {
+            issue(i0 + kVS, vbuf + (ib ^ 1) * WB, nxt);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        // (2) exact row blur of the segment from its entering states: lane (u_me, part)
+        if (u_me < nb) {
+            St1 l, r;
+            float lr[2], li[2], rr_[2], ri[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const float2 lv = cadd(cur.e[j], cmul(f2(pfb[j].x, pfb[j].y), f2(cur.uv[j].x, cur.uv[j].y)));
+                const float2 rv = cadd(cur.bb[j], cmul(f2(pfb[j].z, pfb[j].w), f2(cur.uv[j].z, cur.uv[j].w)));
+                lr[j] = lv.x; li[j] = lv.y; rr_[j] = rv.x; ri[j] = rv.y;
+            }
+            l.ur = f2(lr[0], lr[1]); l.ui = f2(li[0], li[1]);
+            r.ur = f2(rr_[0], rr_[1]); r.ui = f2(ri[0], ri[1]);
+            const int row = u_me * 2 + part;
+            if (Lx == T) blur_line_full(a.row, vb + row * TP, l, r, ob + row * TP);
+            else blur_line<false>(a.row, Lx, vb + row * TP, l, r, ob + row * TP);
+        }
+        __syncwarp();
+        // (3) the scan over the batch, lane = column: the state entering each tile, then past it
+        float2 *dst = A + base + (long long)tile_of(i0, 0) * W;
+        const long long tstride = dir ? -(long long)W : (long long)W;
+#pragma unroll 4
+        for (int u = 0; u < nb; ++u) {
+            const float2 val = f2(ob[(2 * u) * TP + lane], ob[(2 * u + 1) * TP + lane]);
+            const float2 zt = f2(__shfl_sync(0xffffffffu, cur.z.x, u), __shfl_sync(0xffffffffu, cur.z.y, u));
+            if (live) dst[u * tstride] = c;
+            c = cadd(cmul(zt, c), val);
+        }
+        __syncwarp();   // ob and this batch's input buffer are rewritten
+        cur = nxt;
+    }
+    fin[dir * 128 + (threadIdx.x & 127)] = c;   // dir 0: S_tail, dir 1: S_head
+    __syncthreads();
+    if (dir || !live) return;
+    const float2 s_tail = c, s_head = fin[128 + threadIdx.x];
+    const RecAxis &ax = a.col;
+    const float2 zn = k ? f2(ax.znr[1], ax.zni[1]) : f2(ax.znr[0], ax.zni[0]);
+    const float2 inv = k ? f2(ax.invr[1], ax.invi[1]) : f2(ax.invr[0], ax.invi[0]);
+    const float2 um1 = cmul(cadd(s_head, cmul(zn, s_tail)), inv);
+    const float2 vn = cadd(s_tail, cmul(zn, um1));
+    a.UVv[sqk * W + x] = make_float4(um1.x, um1.y, vn.x, vn.y);
+}
+
+cudaError_t launch_vscan(const RecTArgs &a, int NQ, cudaStream_t s) {
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = ensure_smem_attr(rect_vscan_kernel, VScanSmem::BYTES, attr);
+    if (e != cudaSuccess) return e;
+    const long long nsqk = (long long)a.ns * NQ * 2;
+    const long long n = nsqk * a.ntx * 32;
+    rect_vscan_kernel<<<(unsigned)((n + 127) / 128), 256, VScanSmem::BYTES, s>>>(a, NQ, nsqk);
+    return cudaGetLastError();
 }
 
 template <int NP, int MODE>
@@ -612,14 +867,12 @@ cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
     const long long nq = (long long)a.ns * 2 * NP;
     cudaError_t e = launch_tile<NP, 0>(a, a.g1, s);
     if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.nlh, nq, s);
-    if (e == cudaSuccess) {
-        if (a.vl != nullptr) {
-            rect_vline_kernel<NP><<<dim3(((a.ntx + 3) / 4) * a.nty, NP, a.g1), 32, 0, s>>>(a);
-            e = cudaGetLastError();
-        } else {
-            e = launch_tile<NP, 1>(a, a.g1, s);
-        }
+    if (e == cudaSuccess && a.vl != nullptr) {   // rec_impl 2: virtual-line row blur inside the column scan
+        e = launch_vscan(a, 2 * NP, s);
+        if (e == cudaSuccess) e = launch_tile<NP, 2>(a, a.g3, s);
+        return e;
     }
+    if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
     if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
     if (e == cudaSuccess) e = launch_tile<NP, 2>(a, a.g3, s);
     return e;
