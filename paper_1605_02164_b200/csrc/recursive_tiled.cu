@@ -141,7 +141,10 @@ struct TileSmem {
     static constexpr int OFF_RB = OFF_CS + 2 * T * TP;        // cs: [T][TP] float2
     static constexpr int OFF_ZP = OFF_RB + (MODE >= 1 ? NQ * T * TP : 0);   // zp[2 axes][T] float4
     static constexpr int OFF_PFB = OFF_ZP + 2 * 4 * T;   // pfb[2 axes][2 poles] float4 (make_states)
-    static constexpr int OFF_ACC = OFF_PFB + 16;        // MODE 2: acc[NP][T][T]; MODE 0: vs[NP][2][8][TP]
+    // ones: the multiplier of pair 0's planes (cos, sin themselves), so every pair's input is one FMUL2
+    // of (cos, sin) by a plane value -- MODE 0 reads it by row and by column ([T][TP]), MODE >= 1 by row only
+    static constexpr int OFF_ONE = OFF_PFB + 16;
+    static constexpr int OFF_ACC = OFF_ONE + (MODE == 0 ? T * TP : T);   // MODE 2: acc[NP][T][T]; MODE 0: vs[NP][2][8][TP]
     static constexpr size_t BYTES =
         sizeof(float) * (size_t)(OFF_ACC + (MODE == 2 ? NP * T * T : MODE == 0 ? NP * 16 * TP : 0));
 };
@@ -401,12 +404,13 @@ __global__ void __launch_bounds__(32 * NP, tile_min_ctas<NP, MODE>()) rect_tile_
     if (MODE == 2)
         for (int m = 0; m < T; ++m) acc[m * T] = 0.f;
 
-    // the pair's real input at (row i, column j) of the tile
+    float *ones = sm + L::OFF_ONE;
+    for (int e = tid; e < (MODE == 0 ? T * TP : T); e += 32 * NP) ones[e] = 1.f;
+    // the multiplier plane of pair p (pair 0: ones) and the pair's real input at (row i, column j)
+    const float *fpl = (p > 0) ? fs + (p - 1) * T * TP : ones;
     auto xin = [&](int i, int j) -> float2 {
-        const float2 h = cs[i * TP + j];
-        if (p == 0) return h;
-        const float fv = fs[((p - 1) * T + i) * TP + j];
-        return f2(h.x * fv, h.y * fv);
+        const float fv = fpl[i * TP + j];
+        return __fmul2_rn(cs[i * TP + j], f2(fv, fv));
     };
 
     // entering states, software-pipelined: the raw loads of sample b + 1's row (column) states are
@@ -453,12 +457,10 @@ __global__ void __launch_bounds__(32 * NP, tile_min_ctas<NP, MODE>()) rect_tile_
         const bool full = Lx == T && Ly == T;
         if (lane < Ly) {
             const float2 *hrow = cs + lane * TP;
-            const float *frow = fs + ((p > 0 ? p - 1 : 0) * T + lane) * TP;
+            const float *frow = (p > 0 || MODE == 0) ? fpl + lane * TP : ones;   // MODE >= 1: one ones row
             auto xat = [&](int m) -> float2 {   // the pair's real input at column m of this row
-                const float2 h = hrow[m];
-                if (p == 0) return h;
                 const float fv = frow[m];
-                return f2(h.x * fv, h.y * fv);
+                return __fmul2_rn(hrow[m], f2(fv, fv));
             };
             const int y = y0 + lane;
             if (MODE == 0) {
