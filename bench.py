@@ -52,6 +52,8 @@ def parse(argv=None):
     ap.add_argument("--engine", type=int, default=0, help="0 truncated FIR (default), 1 recursive O(1) engine")
     ap.add_argument("--sigma", type=float, default=0.0, help="override the config's sigma_s (engine sweeps)")
     ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled, 2 tiled + virtual lines (default)")
+    ap.add_argument("--rec-tc", type=int, default=-1,
+                    help="engine 1, d = 3: 1 = pass 2's tile blurs on the tensor cores (tcgen05 tf32 x3), 0 = FP32")
     ap.add_argument("--persistent", type=int, default=-1,
                     help="v6 kernel schedule: 1 auto (library default), 0 classic grid, 2 persistent")
     ap.add_argument("--rec-store", type=int, default=-1,
@@ -333,6 +335,8 @@ def run_ours(args, cfg):
         plan.set_option("engine", args.engine)
     if args.rec_impl >= 0:
         plan.set_option("rec_impl", args.rec_impl)
+    if args.rec_tc >= 0:
+        plan.set_option("rec_tc", args.rec_tc)
     if args.rec_store >= 0:
         plan.set_option("rec_store", args.rec_store)
     if args.persistent >= 0:

@@ -131,6 +131,7 @@ cudaError_t launch_recursive(const RecArgs &a, cudaStream_t s);
 // blurred planes never leave the SM. kRecT = tile edge; per axis of nt tiles the plan keeps the
 // pole powers z_j^{L_t}, z_j^{x0_t}, z_j^{n - x0_t - L_t} (fp64-computed, stored fp32 complex).
 constexpr int kRecT = 32;
+constexpr int kRecTcB = 64 * 40;   // tensor-core pass 2: [hi; lo] x (32 Toeplitz + 8 state-basis) columns
 struct RecTabs {
     const float2 *zl;     // [2][nt]
     const float2 *pf;     // [2][nt]
@@ -158,6 +159,9 @@ struct RecTArgs {
     RecTabs th, tv;
     float4 zpc[kRecT];    // (z_0^m, z_1^m), m < kRecT, in the parameter space: full tiles' summaries take
                           // them as uniform constant operands (no per-element shared-memory loads)
+    const float *tcb;     // rec_tc: the tile-blur matrix [K | state basis] (32 x 40, hi / lo tf32 halves) in the
+                          // tensor cores' K-major canonical layout, kRecTcB floats (plan.cu, rec_tc_matrix)
+    int tc;               // rec_tc: pass 2 of full tiles on the tensor cores (d = 3), partial tiles on the FP32 path
     float4 zpq[kRecT];    // the same regrouped (Re z_0^m, Re z_1^m, Im z_0^m, Im z_1^m): both poles of one
                           // real line in one FFMA2 (rec_impl 2's virtual-line summaries)
 };
@@ -222,6 +226,7 @@ struct bf_vec_plan_s {
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
     float *drec = nullptr;     // recursive engine scratch (y1, y2; tiled: summaries)
     int rec_impl = 2;          // recursive engine: 0 staged (row / column passes via HBM), 1 tiled, 2 tiled + virtual lines
+    int rec_tc = 0;            // tiled engine, d = 3: 1 = pass 2's tile blurs as block-Toeplitz GEMMs on the tensor cores
     float2 *drtab = nullptr;   // tiled recursive engine: pole-power tables of both axes
     size_t drtab_n = 0;
     int sampler = 0;           // 0 iid binomial draws (reading R9), 1 stratified (reading R17)

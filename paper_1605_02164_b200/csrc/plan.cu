@@ -718,9 +718,63 @@ bf_status_t ensure_rec_scratch(bf_vec_plan_t p, int nb) {
 
 // Tiled engine: per axis of length n in tiles of kRecT, the pole powers z_j^{L_t}, z_j^{x0_t} and
 // z_j^{n - x0_t - L_t} (each exp(m (-b_j + i w_j) / sigma_s) in fp64), both axes in p->drtab.
+// Tensor-core pass 2 (option rec_tc): the exact blur of a full 32-element segment of a line from its
+// entering states (blur_segment) is one matrix product, y[i] = sum_m K[i][m] x[m] + sum_k S[i][k] s[k],
+// K[i][m] = h(|i - m|) = sum_j Re[A_j z_j^|i-m|] (the Deriche kernel; the diagonal counts the sample
+// once: 2 Re A - g0 = Re A), and the state basis for s = (L_0, L_1, R_0, R_1) as (re, im) pairs,
+// S[i][2j] + i S[i][2j+1] = conj-free split of A_j z_j^{i+1} (L_j) and A_j z_j^{32-i} (R_j):
+// Re[c L] = Re c L.r - Im c L.i. The 32 x 40 matrix B = [K | S] is split into tf32 halves
+// (hi = round-to-nearest tf32, lo = tf32 of the rest) so three tf32 products give fp32 accuracy, and
+// laid out as the MMA's K-major no-swizzle B operand: rows n (0..31 hi, 32..63 lo), core matrices of
+// 8 rows x 4 columns, (n / 8, k / 4) at ((n / 8) * 10 + k / 4) * 32 floats.
+static float tf32_rna(float x) {
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    b = (b + 0x1000u) & ~0x1FFFu;
+    float r;
+    std::memcpy(&r, &b, 4);
+    return r;
+}
+void rec_tc_matrix(double sigma, float *out) {
+    const double a0 = 1.68, a1 = 3.735, b0 = 1.783, b1 = 1.723, c0 = -0.6803, c1 = -0.2598, w0 = 0.6318,
+                 w1 = 1.997;
+    const double bj[2] = {b0, b1}, wj[2] = {w0, w1};
+    Cplx Aj[2] = {{a0, -a1}, {c0, -c1}};
+    double S = -(a0 + c0);
+    Cplx z[2];
+    for (int j = 0; j < 2; ++j) {
+        z[j] = cexp_(-bj[j] / sigma, wj[j] / sigma);
+        S += 2.0 * cdiv(Aj[j], Cplx{1.0 - z[j].r, -z[j].i}).r;
+    }
+    for (int j = 0; j < 2; ++j) Aj[j] = {Aj[j].r / S, Aj[j].i / S};
+    auto azp = [&](int j, int n) {   // A_j z_j^n
+        const Cplx zn = cexp_(-bj[j] * n / sigma, wj[j] * n / sigma);
+        return cmul(Aj[j], zn);
+    };
+    double B[kRecT][40];
+    for (int i = 0; i < kRecT; ++i) {
+        for (int m = 0; m < kRecT; ++m) B[i][m] = azp(0, std::abs(i - m)).r + azp(1, std::abs(i - m)).r;
+        for (int j = 0; j < 2; ++j) {
+            const Cplx l = azp(j, i + 1), r = azp(j, kRecT - i);
+            B[i][32 + 2 * j] = l.r;
+            B[i][33 + 2 * j] = -l.i;
+            B[i][36 + 2 * j] = r.r;
+            B[i][37 + 2 * j] = -r.i;
+        }
+    }
+    for (int n = 0; n < 64; ++n)
+        for (int k = 0; k < 40; ++k) {
+            const int i = n & 31;
+            const float hi = tf32_rna((float)B[i][k]);
+            const float v = n < 32 ? hi : tf32_rna((float)(B[i][k] - (double)hi));
+            out[((n / 8) * 10 + k / 4) * 32 + (n % 8) * 4 + (k % 4)] = v;
+        }
+}
+
 bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
     const int ntx = (p->W + kRecT - 1) / kRecT, nty = (p->H + kRecT - 1) / kRecT;
-    const size_t n = (size_t)6 * (ntx + nty) + 2 * kRecT;   // + zp: (z_0^m, z_1^m), m < kRecT
+    // + zp: (z_0^m, z_1^m), m < kRecT; + the tensor-core tile-blur matrix (kRecTcB floats)
+    const size_t n = (size_t)6 * (ntx + nty) + 2 * kRecT + kRecTcB / 2;
     if (p->drtab_n != n) {
         const double bj[2] = {1.783, 1.723}, wj[2] = {0.6318, 1.997};   // rec_axis's poles
         std::vector<float2> h(n);
@@ -741,6 +795,7 @@ bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
                 const Cplx z = cexp_(-bj[j] * m / p->sigma_s, wj[j] * m / p->sigma_s);
                 h[o++] = make_float2((float)z.r, (float)z.i);
             }
+        rec_tc_matrix(p->sigma_s, reinterpret_cast<float *>(h.data() + o));
         cudaFree(p->drtab);
         p->drtab = nullptr;
         p->drtab_n = 0;
@@ -831,6 +886,8 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     a.rbg = rb_per ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
     a.nlh = nlh;
     a.vl = vlines ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
+    a.tcb = reinterpret_cast<const float *>(a.th.zp + kRecT);
+    a.tc = (p->rec_tc && p->d == 3) ? 1 : 0;
     rec_axis(p->sigma_s, p->W, &a.row);
     rec_axis(p->sigma_s, p->H, &a.col);
     {   // the pole powers z_j^m, m < kRecT (as in ensure_rec_tabs), as kernel parameters
@@ -1620,6 +1677,11 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         p->sampler = (int)v;   // takes effect at the next bf_vec_sample_freqs
         return BF_OK;
     }
+    if (!std::strcmp(name, "rec_tc")) {
+        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        p->rec_tc = (int)v;
+        return BF_OK;
+    }
     if (!std::strcmp(name, "rec_impl")) {
         if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
         p->rec_impl = (int)v;
@@ -1667,7 +1729,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"rec_store", p->rec_store}, {"persistent", p->persistent}, {"last_persistent", p->last_persistent}, {"sampler", p->sampler}, {"colorspace", p->lab},
+        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"rec_tc", p->rec_tc}, {"rec_store", p->rec_store}, {"persistent", p->persistent}, {"last_persistent", p->last_persistent}, {"sampler", p->sampler}, {"colorspace", p->lab},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)

@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(32 * NP, tile_min_ctas<NP, MODE>()) rect_tile_
     const int x0 = tx * T, y0 = ty * T;
     const int H = a.H, W = a.W;
     const int Lx = min(T, W - x0), Ly = min(T, H - y0);
+    if (MODE == 2 && a.tc && Lx == T && Ly == T) return;   // rect_tc2_kernel's tile
     const long long plane = (long long)H * W;
     const int G = (MODE == 2) ? a.g3 : a.g1, g = blockIdx.y;
     const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
@@ -847,6 +848,312 @@ cudaError_t launch_vscan(const RecTArgs &a, int NQ, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Tensor-core pass 2 (option rec_tc, d = 3, full tiles). The exact blur of a full segment from its
+// entering states is linear in (x[0..31], L_0, L_1, R_0, R_1), so a tile's row blur is one product
+//   Y[(q, y)][i] = sum_k A[(q, y)][k] B[i][k],  A = [x row | 8 state reals],  B = [K | state basis]
+// (K[i][m] = h(|i - m|), plan.cu rec_tc_matrix), and the column blur the same with A = [Y column |
+// column states]: per tile and sample M = 256 rows (8 planes x 32 lines, two M = 128 halves), N = 32,
+// K = 40. A lives in tensor memory (written by the line's thread with tcgen05.st), B in shared
+// memory; tf32 operands split into hi + lo halves, A_hi B_hi + A_hi B_lo + A_lo B_hi, give fp32
+// accuracy. One thread issues the 30 MMAs of a blur and commits them to an mbarrier; the 8 warps
+// (warp w: half w / 4, plane 4 (w / 4) + w % 4, lane = line; TMEM lane quarter w % 4) write A, read
+// the result, transpose the row blur through shared memory for the column operand, and fold the
+// column blur into Re[conj(H) blur] in registers (Alg. 1). Same output as pass 2.
+struct TcSmem {
+    static constexpr int OFF_FS = 0;                          // fs[3][T][TP]
+    static constexpr int OFF_CS = 3 * T * TP;                 // cs[T][TP] float2
+    static constexpr int OFF_B = OFF_CS + 2 * T * TP;         // B: [hi; lo] canonical layout, 16 B aligned
+    static constexpr int OFF_TR = OFF_B + kRecTcB;            // transposes [8 warps][T][TP]
+    static constexpr int OFF_PFB = OFF_TR + 8 * T * TP;       // pfb[2 axes][2 poles] float4
+    static constexpr int OFF_BAR = OFF_PFB + 16;              // mbarriers [2 halves], TMEM base
+    static constexpr size_t BYTES = sizeof(float) * (OFF_BAR + 6);
+};
+constexpr int kTcCols = 256;   // D[2] (32 each), A_hi[2] / A_lo[2] (40 each) at 64 + 80 h (+ 40)
+
+struct RawP {   // one plane's entering-state inputs: [pole j]
+    float2 e[2], bb[2];
+    float4 uv[2];
+};
+__device__ __forceinline__ void load_rawp(const float2 *E, const float2 *B, const float4 *UV, int b, int q, int t,
+                                          int line, int nt, int nlines, RawP &r) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        r.e[j] = __ldg(E + sidx(b, q, j, t, line, 8, nt, nlines));
+        r.bb[j] = __ldg(B + sidx(b, q, j, t, line, 8, nt, nlines));
+        r.uv[j] = __ldg(UV + uidx(b, q, j, line, 8, nlines));
+    }
+}
+// x = hi + lo: hi = x rounded to tf32's 10 mantissa bits (half away from zero, two integer ops; the
+// cvt.rna.tf32.f32 instruction is emulated by ~10 instructions on sm_100), lo = the exact fp32
+// remainder, whose low 13 bits the tensor core ignores (error <= 2^-21 |x|)
+__device__ __forceinline__ void tf32_split(float x, uint32_t &hi, uint32_t &lo) {
+    const uint32_t h = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+    hi = h;
+    lo = __float_as_uint(x - __uint_as_float(h));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t t, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(t), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32f(uint32_t t, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(t)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// A row of the operand: 32 line values (val(i)) then the 8 entering-state reals, hi and lo halves
+template <class V>
+__device__ __forceinline__ void tc_write_operand(uint32_t tah, uint32_t tal, V val, const RawP &r,
+                                                 const float4 *pfb) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tf32_split(val(8 * c + j), hi[j], lo[j]);
+        tmem_st8(tah + 8 * c, hi);
+        tmem_st8(tal + 8 * c, lo);
+    }
+    uint32_t hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const float4 pp = pfb[j];
+        const float2 l = cadd(r.e[j], cmul(f2(pp.x, pp.y), f2(r.uv[j].x, r.uv[j].y)));
+        const float2 rr = cadd(r.bb[j], cmul(f2(pp.z, pp.w), f2(r.uv[j].z, r.uv[j].w)));
+        tf32_split(l.x, hi[2 * j], lo[2 * j]);
+        tf32_split(l.y, hi[2 * j + 1], lo[2 * j + 1]);
+        tf32_split(rr.x, hi[4 + 2 * j], lo[4 + 2 * j]);
+        tf32_split(rr.y, hi[5 + 2 * j], lo[5 + 2 * j]);
+    }
+    tmem_st8(tah + 32, hi);
+    tmem_st8(tal + 32, lo);
+}
+// the 15 MMAs of one M half of a blur (5 k-steps, 3 tf32 products), one thread
+__device__ __forceinline__ void tc_blur_mmas(uint32_t tb, uint32_t bm, int h) {
+    constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+    auto desc = [](uint32_t start) -> uint64_t {   // K-major, no swizzle: LBO 128 B (K), SBO 1280 B (N)
+        return (uint64_t)((start >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(1280 >> 4) << 32) |
+               (1ull << 46);
+    };
+    auto mma = [](uint32_t d, uint32_t a, uint64_t b, uint32_t acc) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+            "r"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    };
+    const uint32_t td = tb + 32 * h, tah = tb + 64 + 80 * h, tal = tah + 40;
+#pragma unroll
+    for (int ks = 0; ks < 5; ++ks) {
+        const uint64_t bh = desc(bm + ks * 256), bl = desc(bm + 4 * 1280 + ks * 256);
+        mma(td, tah + 8 * ks, bh, ks > 0 ? 1u : 0u);
+        mma(td, tah + 8 * ks, bl, 1u);
+        mma(td, tal + 8 * ks, bh, 1u);
+    }
+}
+
+// the MMA waits are short (a few hundred cycles): poll without a suspend hint (A/B: BFVEC_TC_SLEEP)
+__device__ __forceinline__ void tc_wait(uint64_t *bar, uint32_t parity) {
+#ifdef BFVEC_TC_SLEEP
+    mbar_wait(bar, parity);
+#else
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(saddr(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+#endif
+}
+
+__global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant__ RecTArgs a) {
+    constexpr int D = 3;
+    extern __shared__ __align__(128) float smt[];
+    float *fs = smt + TcSmem::OFF_FS;
+    float2 *cs = reinterpret_cast<float2 *>(smt + TcSmem::OFF_CS);
+    float *bmat = smt + TcSmem::OFF_B;
+    float *tr = smt + TcSmem::OFF_TR;
+    float4 *pfb = reinterpret_cast<float4 *>(smt + TcSmem::OFF_PFB);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smt + TcSmem::OFF_BAR);
+    uint32_t *tbase_s = reinterpret_cast<uint32_t *>(smt + TcSmem::OFF_BAR + 4);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int half = warp >> 2, qw = warp & 3, q = 4 * half + qw, p = q >> 1, part = q & 1;
+    const int ntxf = a.W / T;
+    const int tx = blockIdx.x % ntxf, ty = blockIdx.x / ntxf;
+    const int x0 = tx * T, y0 = ty * T, H = a.H, W = a.W;
+    const long long plane = (long long)H * W;
+    const int G = a.g3, g = blockIdx.y;
+    const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
+
+    for (int e = tid; e < D * T * T; e += 256) {   // centred f tile (reading R12)
+        const int c = e / (T * T), i = (e / T) % T, j = e % T;
+        fs[(c * T + i) * TP + j] = a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c];
+    }
+    for (int e = tid; e < kRecTcB; e += 256) bmat[e] = __ldg(a.tcb + e);
+    if (tid < 4) {
+        const int ax = tid >> 1, j = tid & 1;
+        const RecTabs &tb = ax ? a.tv : a.th;
+        const int t = ax ? ty : tx, nt = ax ? a.nty : a.ntx;
+        const float2 pf = tb.pf[j * nt + t], pb = tb.pb[j * nt + t];
+        pfb[tid] = make_float4(pf.x, pf.y, pb.x, pb.y);
+    }
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tbase_s)),
+                     "n"(kTcCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // B written by threads, read by the MMAs
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tb = *tbase_s;
+    const uint32_t loff = (uint32_t)(qw * 32) << 16;
+    const uint32_t td = tb + 32 * half + loff, tah = tb + 64 + 80 * half + loff, tal = tah + 40;
+    const uint32_t bm = saddr(bmat);
+
+    float acc[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) acc[i] = 0.f;
+    RawP rraw, craw;
+    float tn[D];
+    if (s0 < s1) {
+        load_rawp(a.Eh, a.Bh, a.UVh, s0, q, tx, y0 + lane, a.ntx, a.nlh, rraw);
+        load_rawp(a.Ev, a.Bv, a.UVv, s0, q, ty, x0 + lane, a.nty, W, craw);
+#pragma unroll
+        for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + s0) * D + c);
+    }
+    uint32_t phase = 0;
+    for (int b = s0; b < s1; ++b) {
+        float tk[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) tk[c] = tn[c];
+        if (b + 1 < s1) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + b + 1) * D + c);
+        }
+        __syncthreads();   // the previous sample is done with cs
+        for (int e = tid; e < T * T; e += 256) {
+            const int i = e / T, j = e % T;
+            float th = 0.f;
+#pragma unroll
+            for (int c = 0; c < D; ++c) th = fmaf(tk[c], fs[(c * T + i) * TP + j], th);
+            float sn, cn;
+            __sincosf(th, &sn, &cn);
+            cs[i * TP + j] = f2(cn, sn);
+        }
+        __syncthreads();
+        // row operand of line (q, y = lane): the pair's modulated plane (Alg. 1) + row states;
+        // part (cos / sin) and pair 0 (no f factor) are warp-uniform: one instance each, no selects
+        {
+            const float *hrow = reinterpret_cast<const float *>(cs + lane * TP) + part;
+            const float *frow = fs + ((p > 0 ? p - 1 : 0) * T + lane) * TP;
+            if (p > 0)
+                tc_write_operand(tah, tal, [&](int m) -> float { return hrow[2 * m] * frow[m]; }, rraw, pfb);
+            else
+                tc_write_operand(tah, tal, [&](int m) -> float { return hrow[2 * m]; }, rraw, pfb);
+        }
+        if (b + 1 < s1) load_rawp(a.Eh, a.Bh, a.UVh, b + 1, q, tx, y0 + lane, a.ntx, a.nlh, rraw);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        named_sync<128>(1 + half);   // the two M halves run as independent pipelines
+        if ((tid & 127) == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            tc_blur_mmas(tb, bm, half);
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             saddr(bar + half))
+                         : "memory");
+        }
+        tc_wait(bar + half, phase);
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // the row blur of line (q, y) -> transpose buffer; column operand of line (q, x = lane)
+        {
+            float y[T];
+            tmem_ld32f(td, y);
+            float *trw = tr + (warp * T + lane) * TP;
+#pragma unroll
+            for (int i = 0; i < T; ++i) trw[i] = y[i];
+        }
+        __syncwarp();
+        {
+            const float *tcol = tr + warp * T * TP + lane;
+            tc_write_operand(tah, tal, [&](int m) -> float { return tcol[m * TP]; }, craw, pfb + 2);
+        }
+        if (b + 1 < s1) load_rawp(a.Ev, a.Bv, a.UVv, b + 1, q, ty, x0 + lane, a.nty, W, craw);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        named_sync<128>(1 + half);   // the two M halves run as independent pipelines
+        if ((tid & 127) == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            tc_blur_mmas(tb, bm, half);
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             saddr(bar + half))
+                         : "memory");
+        }
+        tc_wait(bar + half, phase);
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // the column blur of line (q, x): Re[conj(H) blur] of this plane's part
+        {
+            float z[T];
+            tmem_ld32f(td, z);
+            const float *hcol = reinterpret_cast<const float *>(cs + lane) + part;
+#pragma unroll
+            for (int i = 0; i < T; ++i) acc[i] = fmaf(hcol[2 * i * TP], z[i], acc[i]);
+        }
+        __syncwarp();   // tr is rewritten by the next sample's row blur
+    }
+    // the pair's two planes (warps w, w + 1) summed into the output plane of pair p
+    __syncthreads();
+    if (part) {
+        float *o = tr + warp * T * TP + lane;
+#pragma unroll
+        for (int i = 0; i < T; ++i) o[i * TP] = acc[i];
+    }
+    __syncthreads();
+    if (!part) {
+        const float *o = tr + (warp + 1) * T * TP + lane;
+        const int pl = (p == 0) ? D : p - 1;
+        float *dst = a.pz + ((long long)g * (D + 1) + pl) * plane + (long long)y0 * W + x0 + lane;
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+            const float v = acc[i] + o[i * TP];
+            dst[(long long)i * W] = a.first ? v : dst[(long long)i * W] + v;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(kTcCols) : "memory");
+}
+
+cudaError_t launch_tc2(const RecTArgs &a, cudaStream_t s) {
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = ensure_smem_attr(rect_tc2_kernel, TcSmem::BYTES, attr);
+    if (e != cudaSuccess) return e;
+    rect_tc2_kernel<<<dim3((a.W / T) * (a.H / T), a.g3), 256, TcSmem::BYTES, s>>>(a);
+    return cudaGetLastError();
+}
+
 template <int NP, int MODE>
 cudaError_t launch_tile(const RecTArgs &a, int groups, cudaStream_t s) {
     const size_t smem = TileSmem<NP, MODE>::BYTES;
@@ -871,13 +1178,17 @@ cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
     if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.nlh, nq, s);
     if (e == cudaSuccess && a.vl != nullptr) {   // rec_impl 2: virtual-line row blur inside the column scan
         e = launch_vscan(a, 2 * NP, s);
-        if (e == cudaSuccess) e = launch_tile<NP, 2>(a, a.g3, s);
+    } else {
+        if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
+        if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
+    }
+    if (e != cudaSuccess) return e;
+    if (NP == 4 && a.tc) {   // full tiles on the tensor cores, the rest (if any) on the FP32 path
+        if (a.W % T || a.H % T) e = launch_tile<NP, 2>(a, a.g3, s);
+        if (e == cudaSuccess && a.W >= T && a.H >= T) e = launch_tc2(a, s);
         return e;
     }
-    if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
-    if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
-    if (e == cudaSuccess) e = launch_tile<NP, 2>(a, a.g3, s);
-    return e;
+    return launch_tile<NP, 2>(a, a.g3, s);
 }
 
 }  // namespace

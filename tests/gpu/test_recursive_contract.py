@@ -17,7 +17,7 @@ from workloads.configs import random_image
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("rec_impl", [2, 1, 0])
+@pytest.mark.parametrize("rec_impl", [2, 1, 0, "2tc"])
 @pytest.mark.parametrize("sigma_s", [2.0, 5.0, 10.0])
 def test_recursive_blur_within_half_intensity_of_fir(sigma_s, rec_impl):
     from paper_1605_02164_b200 import Plan
@@ -29,7 +29,8 @@ def test_recursive_blur_within_half_intensity_of_fir(sigma_s, rec_impl):
     for engine in (0, 1):
         p = Plan(H, W, 3, sigma_s, C, 10, 4, 7)
         p.set_option("engine", engine)
-        p.set_option("rec_impl", rec_impl)
+        p.set_option("rec_impl", 2 if rec_impl == "2tc" else rec_impl)
+        p.set_option("rec_tc", 1 if rec_impl == "2tc" else 0)
         p.sample_freqs()
         out[engine] = p.filter(f).cpu().numpy().astype(np.float64)
         p.close()

@@ -17,20 +17,22 @@ from workloads.configs import random_image, small_config
 pytestmark = pytest.mark.gpu
 
 
-_IMPL = {"rec_impl": 1}
+_IMPL = {"rec_impl": 1, "rec_tc": 0}
 
 
-@pytest.fixture(autouse=True, params=[2, 1, 0], ids=["vlines", "tiled", "staged"])
+@pytest.fixture(autouse=True, params=[(2, 0), (2, 1), (1, 0), (0, 0)], ids=["vlines", "vlines_tc", "tiled", "staged"])
 def rec_impl(request):
-    """Every test runs on both implementations of the engine (option "rec_impl")."""
-    _IMPL["rec_impl"] = request.param
-    yield request.param
+    """Every test runs on every implementation of the engine (option "rec_impl"; "rec_tc" = 1: the
+    tiles' pass-2 blurs on the tensor cores, d = 3)."""
+    _IMPL["rec_impl"], _IMPL["rec_tc"] = request.param
+    yield request.param[0]
 
 
 def _rec_plan(cfg, batch=0):
     p = H.gpu_plan(cfg)
     p.set_option("engine", 1)
     p.set_option("rec_impl", _IMPL["rec_impl"])
+    p.set_option("rec_tc", _IMPL["rec_tc"])
     if batch:
         p.set_option("rec_batch", batch)
     return p
