@@ -862,7 +862,7 @@ cudaError_t launch_vscan(const RecTArgs &a, int NQ, cudaStream_t s) {
 // column blur into Re[conj(H) blur] in registers (Alg. 1). Same output as pass 2.
 struct TcSmem {
     static constexpr int OFF_FS = 0;                          // fs[3][T][TP]
-    static constexpr int OFF_CS = 3 * T * TP;                 // cs[T][TP] float2
+    static constexpr int OFF_CS = 3 * T * TP;                 // cs[2][T][TP]: cos plane, sin plane (no bank conflicts)
     static constexpr int OFF_B = OFF_CS + 2 * T * TP;         // B: [hi; lo] canonical layout, 16 B aligned
     static constexpr int OFF_TR = OFF_B + kRecTcB;            // transposes [8 warps][T][TP]
     static constexpr int OFF_PFB = OFF_TR + 8 * T * TP;       // pfb[2 axes][2 poles] float4
@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     constexpr int D = 3;
     extern __shared__ __align__(128) float smt[];
     float *fs = smt + TcSmem::OFF_FS;
-    float2 *cs = reinterpret_cast<float2 *>(smt + TcSmem::OFF_CS);
+    float *cs = smt + TcSmem::OFF_CS;
     float *bmat = smt + TcSmem::OFF_B;
     float *tr = smt + TcSmem::OFF_TR;
     float4 *pfb = reinterpret_cast<float4 *>(smt + TcSmem::OFF_PFB);
@@ -1058,18 +1058,19 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
             for (int c = 0; c < D; ++c) th = fmaf(tk[c], fs[(c * T + i) * TP + j], th);
             float sn, cn;
             __sincosf(th, &sn, &cn);
-            cs[i * TP + j] = f2(cn, sn);
+            cs[i * TP + j] = cn;
+            cs[T * TP + i * TP + j] = sn;
         }
         __syncthreads();
         // row operand of line (q, y = lane): the pair's modulated plane (Alg. 1) + row states;
         // part (cos / sin) and pair 0 (no f factor) are warp-uniform: one instance each, no selects
         {
-            const float *hrow = reinterpret_cast<const float *>(cs + lane * TP) + part;
+            const float *hrow = cs + part * T * TP + lane * TP;
             const float *frow = fs + ((p > 0 ? p - 1 : 0) * T + lane) * TP;
             if (p > 0)
-                tc_write_operand(tah, tal, [&](int m) -> float { return hrow[2 * m] * frow[m]; }, rraw, pfb);
+                tc_write_operand(tah, tal, [&](int m) -> float { return hrow[m] * frow[m]; }, rraw, pfb);
             else
-                tc_write_operand(tah, tal, [&](int m) -> float { return hrow[2 * m]; }, rraw, pfb);
+                tc_write_operand(tah, tal, [&](int m) -> float { return hrow[m]; }, rraw, pfb);
         }
         if (b + 1 < s1) load_rawp(a.Eh, a.Bh, a.UVh, b + 1, q, tx, y0 + lane, a.ntx, a.nlh, rraw);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1116,9 +1117,9 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
         {
             float z[T];
             tmem_ld32f(td, z);
-            const float *hcol = reinterpret_cast<const float *>(cs + lane) + part;
+            const float *hcol = cs + part * T * TP + lane;
 #pragma unroll
-            for (int i = 0; i < T; ++i) acc[i] = fmaf(hcol[2 * i * TP], z[i], acc[i]);
+            for (int i = 0; i < T; ++i) acc[i] = fmaf(hcol[i * TP], z[i], acc[i]);
         }
         __syncwarp();   // tr is rewritten by the next sample's row blur
     }
