@@ -53,7 +53,7 @@ def parse(argv=None):
     ap.add_argument("--sigma", type=float, default=0.0, help="override the config's sigma_s (engine sweeps)")
     ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled, 2 tiled + virtual lines (default)")
     ap.add_argument("--rec-tc", type=int, default=-1,
-                    help="engine 1, d = 3: 1 = pass 2's tile blurs on the tensor cores (tcgen05 tf32 x3), 0 = FP32")
+                    help="engine 1, d = 3: 1 = pass 2's tile blurs on the tensor cores (tcgen05 tf32 x3, the default), 0 = FP32")
     ap.add_argument("--persistent", type=int, default=-1,
                     help="v6 kernel schedule: 1 auto (library default), 0 classic grid, 2 persistent")
     ap.add_argument("--rec-store", type=int, default=-1,
@@ -483,6 +483,9 @@ def run_ours(args, cfg):
         kname = {1: "rect_tile_kernel x3 + rect_scan_kernel x2",
                  2: "rect_tile_kernel x2 + rect_scan_kernel + rect_vscan_kernel"}.get(
                      plan.info("rec_impl"), "rec_row_kernel+rec_col_kernel")
+        if plan.info("rec_impl") >= 1 and plan.info("rec_tc") and cfg.d == 3:
+            kname = kname.replace("rect_tile_kernel x2", "rect_tile_kernel + rect_tc2_kernel")
+            kname = kname.replace("rect_tile_kernel x3", "rect_tile_kernel x2 + rect_tc2_kernel")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": measured_traffic(cfg, kname, units_per_launch,
                                         {"tile_rows": plan.info("tile_rows"), "groups": plan.info("groups"),

@@ -226,7 +226,7 @@ struct bf_vec_plan_s {
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
     float *drec = nullptr;     // recursive engine scratch (y1, y2; tiled: summaries)
     int rec_impl = 2;          // recursive engine: 0 staged (row / column passes via HBM), 1 tiled, 2 tiled + virtual lines
-    int rec_tc = 0;            // tiled engine, d = 3: 1 = pass 2's tile blurs as block-Toeplitz GEMMs on the tensor cores
+    int rec_tc = 1;            // tiled engine, d = 3: 1 = pass 2's tile blurs as block-Toeplitz GEMMs on the tensor cores
     float2 *drtab = nullptr;   // tiled recursive engine: pole-power tables of both axes
     size_t drtab_n = 0;
     int sampler = 0;           // 0 iid binomial draws (reading R9), 1 stratified (reading R17)
