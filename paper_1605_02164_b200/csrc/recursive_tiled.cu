@@ -862,8 +862,8 @@ cudaError_t launch_vscan(const RecTArgs &a, int NQ, cudaStream_t s) {
 // column blur into Re[conj(H) blur] in registers (Alg. 1). Same output as pass 2.
 struct TcSmem {
     static constexpr int OFF_FS = 0;                          // fs[3][T][TP]
-    static constexpr int OFF_CS = 3 * T * TP;                 // cs[2][T][TP]: cos plane, sin plane (no bank conflicts)
-    static constexpr int OFF_B = OFF_CS + 2 * T * TP;         // B: [hi; lo] canonical layout, 16 B aligned
+    static constexpr int OFF_CS = 3 * T * TP;                 // cs[2 samples][2][T][TP]: cos plane, sin plane
+    static constexpr int OFF_B = OFF_CS + 4 * T * TP;         // B: [hi; lo] canonical layout, 16 B aligned
     static constexpr int OFF_TR = OFF_B + kRecTcB;            // transposes [8 warps][T][TP]
     static constexpr int OFF_PFB = OFF_TR + 8 * T * TP;       // pfb[2 axes][2 poles] float4
     static constexpr int OFF_BAR = OFF_PFB + 16;              // mbarriers [2 halves], TMEM base
@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     constexpr int D = 3;
     extern __shared__ __align__(128) float smt[];
     float *fs = smt + TcSmem::OFF_FS;
-    float *cs = smt + TcSmem::OFF_CS;
+    float *csb = smt + TcSmem::OFF_CS;   // double-buffered: sample b in csb + (b & 1) * 2 T TP
     float *bmat = smt + TcSmem::OFF_B;
     float *tr = smt + TcSmem::OFF_TR;
     float4 *pfb = reinterpret_cast<float4 *>(smt + TcSmem::OFF_PFB);
@@ -1041,27 +1041,32 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
 #pragma unroll
         for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + s0) * D + c);
     }
-    uint32_t phase = 0;
-    for (int b = s0; b < s1; ++b) {
-        float tk[D];
-#pragma unroll
-        for (int c = 0; c < D; ++c) tk[c] = tn[c];
-        if (b + 1 < s1) {
-#pragma unroll
-            for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + b + 1) * D + c);
-        }
-        __syncthreads();   // the previous sample is done with cs
+    // (cos, sin) of sample b's phases (Alg. 1) into buffer b & 1: the next sample's
+    // modulation runs while this sample's column blur is on the tensor cores
+    auto modulate = [&](int b, const float (&tk)[D]) {
+        float *c = csb + (b & 1) * 2 * T * TP;
         for (int e = tid; e < T * T; e += 256) {
             const int i = e / T, j = e % T;
             float th = 0.f;
 #pragma unroll
-            for (int c = 0; c < D; ++c) th = fmaf(tk[c], fs[(c * T + i) * TP + j], th);
+            for (int cc = 0; cc < D; ++cc) th = fmaf(tk[cc], fs[(cc * T + i) * TP + j], th);
             float sn, cn;
             __sincosf(th, &sn, &cn);
-            cs[i * TP + j] = cn;
-            cs[T * TP + i * TP + j] = sn;
+            c[i * TP + j] = cn;
+            c[T * TP + i * TP + j] = sn;
         }
-        __syncthreads();
+    };
+    if (s0 < s1) {
+        modulate(s0, tn);
+        if (s0 + 1 < s1) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + s0 + 1) * D + c);
+        }
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (int b = s0; b < s1; ++b) {
+        const float *cs = csb + (b & 1) * 2 * T * TP;
         // row operand of line (q, y = lane): the pair's modulated plane (Alg. 1) + row states;
         // part (cos / sin) and pair 0 (no f factor) are warp-uniform: one instance each, no selects
         {
@@ -1110,6 +1115,13 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
                              saddr(bar + half))
                          : "memory");
         }
+        if (b + 1 < s1) {   // overlaps the column MMAs
+            modulate(b + 1, tn);
+            if (b + 2 < s1) {
+#pragma unroll
+                for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + b + 2) * D + c);
+            }
+        }
         tc_wait(bar + half, phase);
         phase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1121,7 +1133,7 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
 #pragma unroll
             for (int i = 0; i < T; ++i) acc[i] = fmaf(hcol[i * TP], z[i], acc[i]);
         }
-        __syncwarp();   // tr is rewritten by the next sample's row blur
+        __syncthreads();   // sample b + 1's (cos, sin) complete; tr and buffer b & 1 free for reuse
     }
     // the pair's two planes (warps w, w + 1) summed into the output plane of pair p
     __syncthreads();
