@@ -962,10 +962,11 @@ __device__ __forceinline__ void tc_blur_mmas(uint32_t tb, uint32_t bm, int h) {
     }
 }
 
-// the MMA waits are short (a few hundred cycles): poll without a suspend hint (A/B: BFVEC_TC_SLEEP)
+// the MMA waits are short (a few hundred cycles): poll without a suspend hint (A/B: BFVEC_TC_SLEEP,
+// measured equal)
 __device__ __forceinline__ void tc_wait(uint64_t *bar, uint32_t parity) {
-#ifdef BFVEC_TC_SLEEP
-    mbar_wait(bar, parity);
+#if defined(BFVEC_TC_SLEEP) || defined(BFVEC_CHECKED)
+    mbar_wait(bar, parity);   // checked build: with the watchdog
 #else
     uint32_t done;
     do {
