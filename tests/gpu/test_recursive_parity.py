@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 _IMPL = {"rec_impl": 1, "rec_tc": 0}
 
 
-@pytest.fixture(autouse=True, params=[(2, 0), (2, 1), (1, 0), (0, 0)], ids=["vlines", "vlines_tc", "tiled", "staged"])
+@pytest.fixture(autouse=True, params=[(2, 0), (2, 1), (1, 0), (1, 1), (0, 0)],
+                ids=["vlines", "vlines_tc", "tiled", "tiled_tc", "staged"])
 def rec_impl(request):
     """Every test runs on every implementation of the engine (option "rec_impl"; "rec_tc" = 1: the
     tiles' pass-2 blurs on the tensor cores, d = 3)."""
@@ -147,3 +148,26 @@ def test_full_size_config5_sampled_pixels():
     res = H.gates(cfg, S_g[:, ys, xs], P_g[:, ys, xs], Z_g[ys, xs], S_o.T, P_o.T, Z_o)
     print("config 5 (M=4) pixels:", res)
     H.assert_gates(res)
+
+
+@pytest.mark.parametrize("shape", [(256, 256), (200, 328), (64, 1024)])
+def test_tensor_core_pass2_equals_fp32_pass2(shape, rec_impl):
+    """Option rec_tc: pass 2's tile blurs as tf32 x3 GEMMs on the tensor cores give the
+    FP32 recursion's partial sums to fp32 rounding -- on full-tile images and on ragged ones (full
+    tiles on the tensor cores, the rest on the FP32 path). Relative to the largest sum: 2e-6."""
+    if rec_impl == 0 or _IMPL["rec_tc"]:
+        pytest.skip("the staged engine has no pass 2; the _tc fixtures repeat the same comparison")
+    Hh, Ww = shape
+    cfg = dataclasses.replace(CONFIGS[2], H=Hh, W=Ww, M=12)
+    f = torch.from_numpy(random_image(Hh, Ww, 3, seed=Hh + Ww, smooth=True)).cuda()
+    out = {}
+    for tc in (0, 1):
+        p = H.gpu_plan(cfg)
+        p.set_option("engine", 1)
+        p.set_option("rec_impl", rec_impl)
+        p.set_option("rec_tc", tc)
+        out[tc] = p.filter_partial(f, 0, cfg.M).cpu().numpy().astype(np.float64)
+    scale = np.abs(out[0]).max()
+    err = np.abs(out[1] - out[0]).max() / scale
+    print(f"{shape} rec_impl {rec_impl}: max |tc - fp32| / max = {err:.2e}")
+    assert err <= 2e-6
