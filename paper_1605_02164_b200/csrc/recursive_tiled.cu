@@ -143,7 +143,8 @@ struct TileSmem {
     static constexpr int OFF_PFB = OFF_ZP + 2 * 4 * T;   // pfb[2 axes][2 poles] float4 (make_states)
     // ones: the multiplier of pair 0's planes (cos, sin themselves), so every pair's input is one FMUL2
     // of (cos, sin) by a plane value -- MODE 0 reads it by row and by column ([T][TP]), MODE >= 1 by row only
-    static constexpr int OFF_ONE = OFF_PFB + 16;
+    static constexpr int OFF_ZQ = OFF_PFB + 16;           // zpq[T] float4 (MODE 0: virtual-line summaries)
+    static constexpr int OFF_ONE = OFF_ZQ + 4 * T;
     static constexpr int OFF_ACC = OFF_ONE + (MODE == 0 ? T * TP : T);   // MODE 2: acc[NP][T][T]; MODE 0: vs[NP][2][8][TP]
     static constexpr size_t BYTES =
         sizeof(float) * (size_t)(OFF_ACC + (MODE == 2 ? NP * T * T : MODE == 0 ? NP * 16 * TP : 0));
@@ -303,7 +304,7 @@ __device__ __forceinline__ void blur_accumulate(const RecAxis &ax, int n, const 
 // column scan, rect_vscan_kernel) and, through shared memory vs[h][v][TP], into the row summaries of the virtual
 // lines (lane = (h, v), both poles per FFMA2), stored as rows H + 8 ty + v of Eh / Bh.
 template <int NP, class XIN>
-__device__ __forceinline__ void virtual_lines(const RecTArgs &a, float *vs, const float4 *zp, XIN xin, int b, int p,
+__device__ __forceinline__ void virtual_lines(const RecTArgs &a, float *vs, const float4 *zp, const float4 *zq, XIN xin, int b, int p,
                                               int tx, int ty, int lane, int Lx, int Ly, bool full) {
     constexpr int NQ = 2 * NP;
     if (lane < Lx) {
@@ -329,19 +330,41 @@ __device__ __forceinline__ void virtual_lines(const RecTArgs &a, float *vs, cons
             }
     }
     __syncwarp();
-    if (lane < 16) {
+    if (Lx == T) {
+        // full segment: all 32 lanes, lane = (half of the segment, line (h, v)); the two halves'
+        // partial dot products are summed with one shuffle
+        const int hf = lane >> 4, hv = lane & 15, h = hv >> 3, v = hv & 7;
+        const float *row = vs + hv * TP + 16 * hf;
+        float2 er = f2(0.f, 0.f), ei = er, br = er, bi = er;
+#pragma unroll
+        for (int mm = 0; mm < 16; ++mm) {
+            const int m = 16 * hf + mm;
+            const float x = row[mm];
+            const float4 pb = zq[m], pe = zq[T - 1 - m];
+            br = fma2s(x, f2(pb.x, pb.y), br);
+            bi = fma2s(x, f2(pb.z, pb.w), bi);
+            er = fma2s(x, f2(pe.x, pe.y), er);
+            ei = fma2s(x, f2(pe.z, pe.w), ei);
+        }
+        float w[8] = {er.x, er.y, ei.x, ei.y, br.x, br.y, bi.x, bi.y};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] += __shfl_down_sync(0xffffffffu, w[k], 16);
+        if (hf == 0) {
+            const int q = 2 * p + h, line = a.H + ty * 8 + v;
+            a.Eh[sidx(b, q, 0, tx, line, NQ, a.ntx, a.nlh)] = f2(w[0], w[2]);
+            a.Eh[sidx(b, q, 1, tx, line, NQ, a.ntx, a.nlh)] = f2(w[1], w[3]);
+            a.Bh[sidx(b, q, 0, tx, line, NQ, a.ntx, a.nlh)] = f2(w[4], w[6]);
+            a.Bh[sidx(b, q, 1, tx, line, NQ, a.ntx, a.nlh)] = f2(w[5], w[7]);
+        }
+    } else if (lane < 16) {
         const int h = lane >> 3, v = lane & 7;
         const float *row = vs + (h * 8 + v) * TP;
         float2 er, ei, br, bi;
         auto xat = [&](int m) -> float { return row[m]; };
-        if (Lx == T) {
-            summaries_line<true>(T, xat, [&](int m) -> float4 { return a.zpq[m]; }, er, ei, br, bi);
-        } else {
-            summaries_line<false>(Lx, xat, [&](int m) -> float4 {
-                const float4 z = zp[m];
-                return make_float4(z.x, z.z, z.y, z.w);
-            }, er, ei, br, bi);
-        }
+        summaries_line<false>(Lx, xat, [&](int m) -> float4 {
+            const float4 z = zp[m];
+            return make_float4(z.x, z.z, z.y, z.w);
+        }, er, ei, br, bi);
         const int q = 2 * p + h, line = a.H + ty * 8 + v;
         a.Eh[sidx(b, q, 0, tx, line, NQ, a.ntx, a.nlh)] = f2(er.x, ei.x);
         a.Eh[sidx(b, q, 1, tx, line, NQ, a.ntx, a.nlh)] = f2(er.y, ei.y);
@@ -405,6 +428,8 @@ __global__ void __launch_bounds__(32 * NP, tile_min_ctas<NP, MODE>()) rect_tile_
     if (MODE == 2)
         for (int m = 0; m < T; ++m) acc[m * T] = 0.f;
 
+    float4 *zq = reinterpret_cast<float4 *>(sm + L::OFF_ZQ);   // (Re z_0^m, Re z_1^m, Im z_0^m, Im z_1^m)
+    if (MODE == 0 && tid < T) zq[tid] = a.zpq[tid];
     float *ones = sm + L::OFF_ONE;
     for (int e = tid; e < (MODE == 0 ? T * TP : T); e += 32 * NP) ones[e] = 1.f;
     // the multiplier plane of pair p (pair 0: ones) and the pair's real input at (row i, column j)
@@ -478,7 +503,7 @@ __global__ void __launch_bounds__(32 * NP, tile_min_ctas<NP, MODE>()) rect_tile_
             }
         }
         if (MODE == 0) {
-            if (a.vl != nullptr) virtual_lines<NP>(a, sm + L::OFF_ACC + p * 16 * TP, zp, xin, b, p, tx, ty, lane,
+            if (a.vl != nullptr) virtual_lines<NP>(a, sm + L::OFF_ACC + p * 16 * TP, zp, zq, xin, b, p, tx, ty, lane,
                                                    Lx, Ly, full);
             continue;
         }
