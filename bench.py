@@ -54,6 +54,8 @@ def parse(argv=None):
     ap.add_argument("--rec-impl", type=int, default=-1, help="engine 1: 0 staged passes, 1 tiled, 2 tiled + virtual lines (default)")
     ap.add_argument("--rec-tc", type=int, default=-1,
                     help="engine 1, d = 3: 1 = pass 2's tile blurs on the tensor cores (tcgen05 tf32 x3, the default), 0 = FP32")
+    ap.add_argument("--rec-vtc", type=int, default=-1,
+                    help="engine 1 with --rec-tc 1: 1 = the column scan's virtual-line blurs on the tensor cores too (default)")
     ap.add_argument("--persistent", type=int, default=-1,
                     help="v6 kernel schedule: 1 auto (library default), 0 classic grid, 2 persistent")
     ap.add_argument("--rec-store", type=int, default=-1,
@@ -337,6 +339,8 @@ def run_ours(args, cfg):
         plan.set_option("rec_impl", args.rec_impl)
     if args.rec_tc >= 0:
         plan.set_option("rec_tc", args.rec_tc)
+    if args.rec_vtc >= 0:
+        plan.set_option("rec_vtc", args.rec_vtc)
     if args.rec_store >= 0:
         plan.set_option("rec_store", args.rec_store)
     if args.persistent >= 0:
@@ -483,6 +487,9 @@ def run_ours(args, cfg):
         kname = {1: "rect_tile_kernel x3 + rect_scan_kernel x2",
                  2: "rect_tile_kernel x2 + rect_scan_kernel + rect_vscan_kernel"}.get(
                      plan.info("rec_impl"), "rec_row_kernel+rec_col_kernel")
+        if plan.info("rec_impl") == 2 and plan.info("rec_tc") and plan.info("rec_vtc") and cfg.d == 3 \
+                and cfg.W % 32 == 0:
+            kname = kname.replace("rect_vscan_kernel", "rect_vscan_tc_kernel")
         if plan.info("rec_impl") >= 1 and plan.info("rec_tc") and cfg.d == 3:
             kname = kname.replace("rect_tile_kernel x2", "rect_tile_kernel + rect_tc2_kernel")
             kname = kname.replace("rect_tile_kernel x3", "rect_tile_kernel x2 + rect_tc2_kernel")

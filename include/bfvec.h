@@ -331,6 +331,8 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 Toeplitz block), run as tcgen05.mma kind::tf32 with operands split into tf32
  *                 hi + lo halves (three products, fp32 accuracy); partial tiles and d != 3 use the
  *                 FP32 recursion. 0: FP32 recursion everywhere. Results equal to fp32 rounding.
+ *   "rec_vtc"     with rec_tc = 1, rec_impl 2 and W a multiple of 32: 1 (default) the column
+ *                 scan's virtual-line segment blurs run as the same tensor-core product; 0 FP32.
  *   "rec_store"   engine 1, rec_impl 1 (ignored by 2): 1 pass 1 stores its exact row blur (2(d+1) fp32 planes per
  *                 sample in flight) and pass 2 reads it instead of recomputing it; 0 (default)
  *                 recompute (measured 2 % faster on config 5)
@@ -359,7 +361,7 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t plan, const char *name, double value
  *   "radius", "d", "H", "W", "M", "N", "tile_rows", "groups", "ctas",
  *   "launches_per_filter", "smem_bytes", "threads", "kernel_D", "kernel_R",
  *   "regs", "occupancy", "alias", "variant", "spatial_kernel", "engine", "rec_batch" (last batch
- *   size), "rec_impl", "rec_tc", "fir_supported" (r <= 64), "sampler", "colorspace", "graph", "graph_ready", and (option "profile") "fused_ns_total",
+ *   size), "rec_impl", "rec_tc", "rec_vtc", "fir_supported" (r <= 64), "sampler", "colorspace", "graph", "graph_ready", and (option "profile") "fused_ns_total",
  *   "fused_calls" (synchronises on the recorded events). Returns BF_E_ARG for
  *   an unknown name.
  */

@@ -888,6 +888,7 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     a.vl = vlines ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
     a.tcb = reinterpret_cast<const float *>(a.th.zp + kRecT);
     a.tc = (p->rec_tc && p->d == 3) ? 1 : 0;
+    a.vtc = (p->rec_vtc && a.tc && p->W % kRecT == 0) ? 1 : 0;
     rec_axis(p->sigma_s, p->W, &a.row);
     rec_axis(p->sigma_s, p->H, &a.col);
     {   // the pole powers z_j^m, m < kRecT (as in ensure_rec_tabs), as kernel parameters
@@ -1677,6 +1678,11 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         p->sampler = (int)v;   // takes effect at the next bf_vec_sample_freqs
         return BF_OK;
     }
+    if (!std::strcmp(name, "rec_vtc")) {   // A/B: the column scan's virtual-line blurs on the tensor cores
+        if (v != 0.0 && v != 1.0) return BF_E_ARG;
+        p->rec_vtc = (int)v;
+        return BF_OK;
+    }
     if (!std::strcmp(name, "rec_tc")) {
         if (v != 0.0 && v != 1.0) return BF_E_ARG;
         p->rec_tc = (int)v;
@@ -1729,7 +1735,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"rec_tc", p->rec_tc}, {"rec_store", p->rec_store}, {"persistent", p->persistent}, {"last_persistent", p->last_persistent}, {"sampler", p->sampler}, {"colorspace", p->lab},
+        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"rec_tc", p->rec_tc}, {"rec_vtc", p->rec_vtc}, {"rec_store", p->rec_store}, {"persistent", p->persistent}, {"last_persistent", p->last_persistent}, {"sampler", p->sampler}, {"colorspace", p->lab},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)

@@ -1193,6 +1193,212 @@ cudaError_t launch_tc2(const RecTArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// rec_impl 2 + rec_tc: the column scan with the virtual lines' segment blurs on the tensor cores.
+// Same work decomposition as rect_vscan_kernel (warp = 32 columns of one tile column, one (sample,
+// plane, column pole) and direction; batches of kVS tile rows); the 32 segments a warp blurs per
+// batch (lane (u, part)) are rows of the pass-2 product [x | entering states] x [K | state basis]
+// (the row axis' B, rec_tc_matrix), the 4 warps of a direction form one M = 128 half: operands by
+// tcgen05.st, 15 MMAs issued by one thread, the result read back with tcgen05.ld into the batch's
+// (now consumed) input buffer, which the scan then reads. Full tile columns only (W % 32 == 0; the
+// plan keeps rect_vscan_kernel otherwise). Every warp takes part in every MMA round (named barrier
+// per direction), live or not.
+struct VScanTcSmem {
+    static constexpr int WARPS = 8, ROWS = 2 * kVS, WB = ROWS * TP;
+    static constexpr int OFF_VB = 0;                              // [8 warps][2][ROWS][TP]
+    static constexpr int OFF_B = OFF_VB + WARPS * 2 * WB;         // B [hi; lo], 16 B aligned
+    static constexpr int OFF_FIN = OFF_B + kRecTcB;               // fin [2][128] float2
+    static constexpr int OFF_BAR = OFF_FIN + 2 * 2 * 128;         // mbarriers [2], TMEM base
+    static constexpr size_t BYTES = sizeof(float) * (OFF_BAR + 6);
+};
+
+__global__ void __launch_bounds__(256, 2) rect_vscan_tc_kernel(const __grid_constant__ RecTArgs a, int NQ,
+                                                               long long nsqk) {
+    extern __shared__ __align__(128) float smq[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int WB = VScanTcSmem::WB;
+    float *vbuf = smq + VScanTcSmem::OFF_VB + warp * 2 * WB;
+    const int dir = tid >> 7, qw = warp & 3;
+    float *bmat = smq + VScanTcSmem::OFF_B;
+    float2 *fin = reinterpret_cast<float2 *>(smq + VScanTcSmem::OFF_FIN);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smq + VScanTcSmem::OFF_BAR);
+    uint32_t *tbase_s = reinterpret_cast<uint32_t *>(smq + VScanTcSmem::OFF_BAR + 4);
+    const int ntx = a.ntx, nty = a.nty, W = a.W;
+    const long long id = (long long)blockIdx.x * 128 + (tid & 127);
+    const long long per = (long long)ntx * 32;
+    const long long sqk = id / per;
+    const int tx = (int)((id % per) >> 5);
+    const int x0 = tx * T, x = x0 + lane;
+    const bool wlive = sqk < nsqk;   // warp-uniform
+    const bool live = wlive && x < W;
+    const int Lx = min(T, W - x0);
+    const int k = (int)(sqk & 1);
+    const long long sq = sqk >> 1;
+    const int q = (int)(sq % NQ), s = (int)(sq / NQ);
+    const int u_me = lane & 15, part = lane >> 4, v_me = (k * 2 + dir) * 2 + part;
+
+    for (int e = tid; e < kRecTcB; e += 256) bmat[e] = __ldg(a.tcb + e);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tbase_s)),
+                     "n"(kTcCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tb = *tbase_s;
+    const uint32_t loff = (uint32_t)(qw * 32) << 16;
+    const uint32_t td = tb + 32 * dir + loff, tah = tb + 64 + 80 * dir + loff, tal = tah + 40;
+    const uint32_t bm = saddr(bmat);
+
+    float4 pfb[2];
+    if (wlive) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float2 pf = a.th.pf[j * ntx + tx], pb = a.th.pb[j * ntx + tx];
+            pfb[j] = make_float4(pf.x, pf.y, pb.x, pb.y);
+        }
+    }
+    float2 *A = dir ? a.Bv : a.Ev;
+    const long long base = sqk * nty * (long long)W + x;
+    const float2 *zl = a.tv.zl + k * nty;
+    auto tile_of = [&](int i0, int u) { return dir ? nty - 1 - (i0 + u) : i0 + u; };
+    auto issue = [&](int i0, float *vb, VBatch &nx) {
+        if (!wlive) {
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            return;
+        }
+        const int nb = min(kVS, nty - i0);
+        const float *src0 = a.vl + vlidx(s, q, tile_of(i0, 0), (k * 2 + dir) * 2, min(x, W - 1), NQ, nty, W);
+        const int ustride = (dir ? -8 : 8) * W;
+        const unsigned dst0 = (unsigned)__cvta_generic_to_shared(vb + lane);
+        const int bytes = lane < Lx ? 4 : 0;
+        const float *sp = src0;
+#pragma unroll
+        for (int u = 0; u < kVS; ++u) {
+            if (u < nb) {
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst0 + 8u * u * TP), "l"(sp),
+                             "r"(bytes)
+                             : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst0 + 4u * (2 * u + 1) * TP),
+                             "l"(sp + W), "r"(bytes)
+                             : "memory");
+            }
+            sp += ustride;
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (u_me < nb) {
+            const int t = tile_of(i0, u_me);
+            const int line = a.H + t * 8 + v_me;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                nx.e[j] = __ldg(a.Eh + sidx(s, q, j, tx, line, NQ, ntx, a.nlh));
+                nx.bb[j] = __ldg(a.Bh + sidx(s, q, j, tx, line, NQ, ntx, a.nlh));
+                nx.uv[j] = __ldg(a.UVh + uidx(s, q, j, line, NQ, a.nlh));
+            }
+            nx.z = zl[t];
+        } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                nx.e[j] = nx.bb[j] = f2(0.f, 0.f);
+                nx.uv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            nx.z = f2(0.f, 0.f);
+        }
+    };
+    float2 c = f2(0.f, 0.f);
+    VBatch cur, nxt;
+    issue(0, vbuf, cur);
+    uint32_t phase = 0;
+    for (int i0 = 0, ib = 0; i0 < nty; i0 += kVS, ib ^= 1) {
+        const int nb = min(kVS, nty - i0);
+        float *vb = vbuf + ib * WB;
+        if (i0 + kVS < nty) {
+            issue(i0 + kVS, vbuf + (ib ^ 1) * WB, nxt);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+        const int row = u_me * 2 + part;
+        // the operand: this lane's segment (32 values) and its entering states, tf32 hi / lo
+        {
+            RawP r;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                r.e[j] = cur.e[j];
+                r.bb[j] = cur.bb[j];
+                r.uv[j] = cur.uv[j];
+            }
+            const float *xr = vb + row * TP;
+            tc_write_operand(tah, tal, [&](int m) -> float { return xr[m]; }, r, pfb);
+        }
+        const float *ob = vb;   // consumed: the blurred segments go back into it
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        named_sync<128>(1 + dir);
+        if ((tid & 127) == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            tc_blur_mmas(tb, bm, dir);
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             saddr(bar + dir))
+                         : "memory");
+        }
+        tc_wait(bar + dir, phase);
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        {
+            float y[T];
+            tmem_ld32f(td, y);
+            float *yr = vb + row * TP;
+#pragma unroll
+            for (int i = 0; i < T; ++i) yr[i] = y[i];
+        }
+        __syncwarp();
+        // the scan over the batch, lane = column
+        float2 *dst = A + base + (long long)tile_of(i0, 0) * W;
+        const long long tstride = dir ? -(long long)W : (long long)W;
+#pragma unroll 4
+        for (int u = 0; u < nb; ++u) {
+            const float2 val = f2(ob[(2 * u) * TP + lane], ob[(2 * u + 1) * TP + lane]);
+            const float2 zt = f2(__shfl_sync(0xffffffffu, cur.z.x, u), __shfl_sync(0xffffffffu, cur.z.y, u));
+            if (live) dst[u * tstride] = c;
+            c = cadd(cmul(zt, c), val);
+        }
+        __syncwarp();
+        cur = nxt;
+    }
+    fin[dir * 128 + (tid & 127)] = c;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(kTcCols) : "memory");
+    if (dir || !live) return;
+    const float2 s_tail = c, s_head = fin[128 + tid];
+    const RecAxis &ax = a.col;
+    const float2 zn = k ? f2(ax.znr[1], ax.zni[1]) : f2(ax.znr[0], ax.zni[0]);
+    const float2 inv = k ? f2(ax.invr[1], ax.invi[1]) : f2(ax.invr[0], ax.invi[0]);
+    const float2 um1 = cmul(cadd(s_head, cmul(zn, s_tail)), inv);
+    const float2 vn = cadd(s_tail, cmul(zn, um1));
+    a.UVv[sqk * W + x] = make_float4(um1.x, um1.y, vn.x, vn.y);
+}
+
+cudaError_t launch_vscan_tc(const RecTArgs &a, int NQ, cudaStream_t s) {
+    static std::atomic<uint64_t> attr{0};
+    cudaError_t e = ensure_smem_attr(rect_vscan_tc_kernel, VScanTcSmem::BYTES, attr);
+    if (e != cudaSuccess) return e;
+    const long long nsqk = (long long)a.ns * NQ * 2;
+    const long long n = nsqk * a.ntx * 32;
+    rect_vscan_tc_kernel<<<(unsigned)((n + 127) / 128), 256, VScanTcSmem::BYTES, s>>>(a, NQ, nsqk);
+    return cudaGetLastError();
+}
+
 template <int NP, int MODE>
 cudaError_t launch_tile(const RecTArgs &a, int groups, cudaStream_t s) {
     const size_t smem = TileSmem<NP, MODE>::BYTES;
@@ -1216,7 +1422,7 @@ cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
     cudaError_t e = launch_tile<NP, 0>(a, a.g1, s);
     if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.nlh, nq, s);
     if (e == cudaSuccess && a.vl != nullptr) {   // rec_impl 2: virtual-line row blur inside the column scan
-        e = launch_vscan(a, 2 * NP, s);
+        e = (a.tc && a.vtc) ? launch_vscan_tc(a, 2 * NP, s) : launch_vscan(a, 2 * NP, s);
     } else {
         if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
         if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);

@@ -17,15 +17,16 @@ from workloads.configs import random_image, small_config
 pytestmark = pytest.mark.gpu
 
 
-_IMPL = {"rec_impl": 1, "rec_tc": 0}
+_IMPL = {"rec_impl": 1, "rec_tc": 0, "rec_vtc": 0}
 
 
-@pytest.fixture(autouse=True, params=[(2, 0), (2, 1), (1, 0), (1, 1), (0, 0)],
-                ids=["vlines", "vlines_tc", "tiled", "tiled_tc", "staged"])
+@pytest.fixture(autouse=True, params=[(2, 0, 0), (2, 1, 0), (2, 1, 1), (1, 0, 0), (1, 1, 0), (0, 0, 0)],
+                ids=["vlines", "vlines_tc", "vlines_tc_vscan", "tiled", "tiled_tc", "staged"])
 def rec_impl(request):
     """Every test runs on every implementation of the engine (option "rec_impl"; "rec_tc" = 1: the
-    tiles' pass-2 blurs on the tensor cores, d = 3)."""
-    _IMPL["rec_impl"], _IMPL["rec_tc"] = request.param
+    tiles' pass-2 blurs on the tensor cores, d = 3; "rec_vtc" = 1: the column scan's virtual-line
+    blurs too, W a multiple of 32)."""
+    _IMPL["rec_impl"], _IMPL["rec_tc"], _IMPL["rec_vtc"] = request.param
     yield request.param[0]
 
 
@@ -34,6 +35,7 @@ def _rec_plan(cfg, batch=0):
     p.set_option("engine", 1)
     p.set_option("rec_impl", _IMPL["rec_impl"])
     p.set_option("rec_tc", _IMPL["rec_tc"])
+    p.set_option("rec_vtc", _IMPL["rec_vtc"])
     if batch:
         p.set_option("rec_batch", batch)
     return p
