@@ -1138,7 +1138,10 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     // engine 1 per batch: staged 2 kernels (row, column), tiled 5 (3 tile passes, 2 scans), tiled with
     // virtual lines 4 (2 tile passes, 2 scans)
     // engine 0: pad, fused kernel (variant 8: two launches), diagnostics reset, normalise
-    p->last_launches = ((p->engine == 1) ? 2 + (p->rec_impl == 2 ? 4 : p->rec_impl == 1 ? 5 : 2) *
+    // tensor-core pass 2 on an image with partial tiles: + the FP32 pass 2 for those tiles
+    const int tc_split = (p->engine == 1 && p->rec_impl >= 1 && p->rec_tc && p->d == 3 &&
+                          (p->W % kRecT || p->H % kRecT) && p->W >= kRecT && p->H >= kRecT) ? 1 : 0;
+    p->last_launches = ((p->engine == 1) ? 2 + ((p->rec_impl == 2 ? 4 : p->rec_impl == 1 ? 5 : 2) + tc_split) *
                                                    ((p->M + p->last_batch - 1) / p->last_batch)
                                          : 4 + (p->kinfo.variant == 8 ? 1 : 0)) + (p->lab ? 2 : 0);
     p->last = s;
