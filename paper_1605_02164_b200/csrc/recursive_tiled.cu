@@ -378,9 +378,12 @@ __device__ __forceinline__ void virtual_lines(const RecTArgs &a, float *vs, cons
 #ifndef BFVEC_REC_P2CTAS
 #define BFVEC_REC_P2CTAS 3   // pass 2 is limited to 3 CTAs per SM by its 72 KB of shared memory anyway (A/B: 21.9 -> 21.2 ms)
 #endif
+#ifndef BFVEC_REC_P0CTAS
+#define BFVEC_REC_P0CTAS 4   // A/B: 5 CTAs 8.53 ms, 6 CTAs 8.94 ms (spills) vs 8.09 ms
+#endif
 template <int NP, int MODE>
 constexpr int tile_min_ctas() {
-    return NP <= 4 ? (MODE == 2 ? BFVEC_REC_P2CTAS : 4) : (MODE == 0 || NP <= 7) ? 2 : 1;
+    return NP <= 4 ? (MODE == 2 ? BFVEC_REC_P2CTAS : MODE == 0 ? BFVEC_REC_P0CTAS : 4) : (MODE == 0 || NP <= 7) ? 2 : 1;
 }
 // A/B: BFVEC_REC_EAGER turns the raw entering-state loads into states right at the load (as before
 // round 2's change) instead of at the use
