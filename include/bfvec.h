@@ -325,14 +325,15 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 every tile to form the column summaries; 0 staged -- a row pass and a column
  *                 pass through HBM scratch. Same arithmetic, results equal to fp32 rounding
  *                 (all three gated against the oracle).
- *   "rec_tc"      engine 1, tiled, d = 3: 1 (default) pass 2 blurs every full 32 x 32 tile on the
+ *   "rec_tc"      engine 1, tiled, d <= 7: 1 (default) pass 2 blurs every full 32 x 32 tile on the
  *                 tensor cores -- the exact blur of a segment from its entering states is one
  *                 product [x | states] x [K | state basis] (K = the Deriche kernel's 32 x 32
  *                 Toeplitz block), run as tcgen05.mma kind::tf32 with operands split into tf32
- *                 hi + lo halves (three products, fp32 accuracy); partial tiles and d != 3 use the
- *                 FP32 recursion. 0: FP32 recursion everywhere. Results equal to fp32 rounding.
- *   "rec_vtc"     with rec_tc = 1, rec_impl 2 and W a multiple of 32: 1 (default) the column
- *                 scan's virtual-line segment blurs run as the same tensor-core product; 0 FP32.
+ *                 hi + lo halves (three products, fp32 accuracy), ceil(2(d+1)/4) M = 128 halves
+ *                 of four planes; partial tiles and d = 8 use the FP32 recursion. 0: FP32
+ *                 recursion everywhere. Results equal to fp32 rounding.
+ *   "rec_vtc"     with rec_tc = 1, rec_impl 2 and W a multiple of 32 (any d): 1 (default) the
+ *                 column scan's virtual-line segment blurs run as the same tensor-core product.
  *   "rec_store"   engine 1, rec_impl 1 (ignored by 2): 1 pass 1 stores its exact row blur (2(d+1) fp32 planes per
  *                 sample in flight) and pass 2 reads it instead of recomputing it; 0 (default)
  *                 recompute (measured 2 % faster on config 5)

@@ -161,7 +161,7 @@ struct RecTArgs {
                           // them as uniform constant operands (no per-element shared-memory loads)
     const float *tcb;     // rec_tc: the tile-blur matrix [K | state basis] (32 x 40, hi / lo tf32 halves) in the
                           // tensor cores' K-major canonical layout, kRecTcB floats (plan.cu, rec_tc_matrix)
-    int tc;               // rec_tc: pass 2 of full tiles on the tensor cores (d = 3), partial tiles on the FP32 path
+    int tc;               // rec_tc: pass 2 of full tiles on the tensor cores (d <= 7), partial tiles on the FP32 path
     int vtc;              // rec_tc, rec_impl 2: the virtual lines' segment blurs on the tensor cores too
     float4 zpq[kRecT];    // the same regrouped (Re z_0^m, Re z_1^m, Im z_0^m, Im z_1^m): both poles of one
                           // real line in one FFMA2 (rec_impl 2's virtual-line summaries)
@@ -227,7 +227,7 @@ struct bf_vec_plan_s {
     int force_batch = 0;       // recursive engine: samples per batch (0 = auto)
     float *drec = nullptr;     // recursive engine scratch (y1, y2; tiled: summaries)
     int rec_impl = 2;          // recursive engine: 0 staged (row / column passes via HBM), 1 tiled, 2 tiled + virtual lines
-    int rec_tc = 1;            // tiled engine, d = 3: 1 = pass 2's tile blurs as block-Toeplitz GEMMs on the tensor cores
+    int rec_tc = 1;            // tiled engine: 1 = pass 2's tile blurs (d <= 7) as block-Toeplitz GEMMs on the tensor cores
     int rec_vtc = 1;           // with rec_tc: the column scan's virtual-line segment blurs on the tensor cores too
     float2 *drtab = nullptr;   // tiled recursive engine: pole-power tables of both axes
     size_t drtab_n = 0;

@@ -887,8 +887,8 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     a.nlh = nlh;
     a.vl = vlines ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
     a.tcb = reinterpret_cast<const float *>(a.th.zp + kRecT);
-    a.tc = (p->rec_tc && p->d == 3) ? 1 : 0;
-    a.vtc = (p->rec_vtc && a.tc && p->W % kRecT == 0) ? 1 : 0;
+    a.tc = (p->rec_tc && p->d <= 7) ? 1 : 0;   // up to four M halves (16 planes) in tensor memory
+    a.vtc = (p->rec_vtc && p->rec_tc && p->W % kRecT == 0) ? 1 : 0;
     rec_axis(p->sigma_s, p->W, &a.row);
     rec_axis(p->sigma_s, p->H, &a.col);
     {   // the pole powers z_j^m, m < kRecT (as in ensure_rec_tabs), as kernel parameters
@@ -1139,7 +1139,7 @@ static bf_status_t filter_band(bf_vec_plan_t p, const float *slab, int slab_rows
     // virtual lines 4 (2 tile passes, 2 scans)
     // engine 0: pad, fused kernel (variant 8: two launches), diagnostics reset, normalise
     // tensor-core pass 2 on an image with partial tiles: + the FP32 pass 2 for those tiles
-    const int tc_split = (p->engine == 1 && p->rec_impl >= 1 && p->rec_tc && p->d == 3 &&
+    const int tc_split = (p->engine == 1 && p->rec_impl >= 1 && p->rec_tc && p->d <= 7 &&
                           (p->W % kRecT || p->H % kRecT) && p->W >= kRecT && p->H >= kRecT) ? 1 : 0;
     p->last_launches = ((p->engine == 1) ? 2 + ((p->rec_impl == 2 ? 4 : p->rec_impl == 1 ? 5 : 2) + tc_split) *
                                                    ((p->M + p->last_batch - 1) / p->last_batch)

@@ -888,14 +888,18 @@ cudaError_t launch_vscan(const RecTArgs &a, int NQ, cudaStream_t s) {
 // (warp w: half w / 4, plane 4 (w / 4) + w % 4, lane = line; TMEM lane quarter w % 4) write A, read
 // the result, transpose the row blur through shared memory for the column operand, and fold the
 // column blur into Re[conj(H) blur] in registers (Alg. 1). Same output as pass 2.
+// NP pairs -> NQ = 2 NP planes in NH = ceil(NQ / 4) M halves of 4 planes (the last one padded)
+template <int NP>
 struct TcSmem {
-    static constexpr int OFF_FS = 0;                          // fs[3][T][TP]
-    static constexpr int OFF_CS = 3 * T * TP;                 // cs[2 samples][2][T][TP]: cos plane, sin plane
+    static constexpr int D = NP - 1, NQ = 2 * NP, NH = (NQ + 3) / 4, WARPS = 4 * NH;
+    static constexpr int OFF_FS = 0;                          // fs[D][T][TP]
+    static constexpr int OFF_CS = D * T * TP;                 // cs[2 samples][2][T][TP]: cos plane, sin plane
     static constexpr int OFF_B = OFF_CS + 4 * T * TP;         // B: [hi; lo] canonical layout, 16 B aligned
-    static constexpr int OFF_TR = OFF_B + kRecTcB;            // transposes [8 warps][T][TP]
-    static constexpr int OFF_PFB = OFF_TR + 8 * T * TP;       // pfb[2 axes][2 poles] float4
-    static constexpr int OFF_BAR = OFF_PFB + 16;              // mbarriers [2 halves], TMEM base
-    static constexpr size_t BYTES = sizeof(float) * (OFF_BAR + 6);
+    static constexpr int OFF_TR = OFF_B + kRecTcB;            // transposes [WARPS][T][TP]
+    static constexpr int OFF_PFB = OFF_TR + WARPS * T * TP;   // pfb[2 axes][2 poles] float4
+    static constexpr int OFF_BAR = OFF_PFB + 16;              // mbarriers [NH], TMEM base
+    static constexpr size_t BYTES = sizeof(float) * (OFF_BAR + 2 * NH + 2);
+    static constexpr int COLS = NH <= 2 ? 256 : 512;          // tensor memory: 112 columns per half
 };
 constexpr int kTcCols = 256;   // D[2] (32 each), A_hi[2] / A_lo[2] (40 each) at 64 + 80 h (+ 40)
 
@@ -903,13 +907,14 @@ struct RawP {   // one plane's entering-state inputs: [pole j]
     float2 e[2], bb[2];
     float4 uv[2];
 };
+template <int NQ>
 __device__ __forceinline__ void load_rawp(const float2 *E, const float2 *B, const float4 *UV, int b, int q, int t,
                                           int line, int nt, int nlines, RawP &r) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        r.e[j] = __ldg(E + sidx(b, q, j, t, line, 8, nt, nlines));
-        r.bb[j] = __ldg(B + sidx(b, q, j, t, line, 8, nt, nlines));
-        r.uv[j] = __ldg(UV + uidx(b, q, j, line, 8, nlines));
+        r.e[j] = __ldg(E + sidx(b, q, j, t, line, NQ, nt, nlines));
+        r.bb[j] = __ldg(B + sidx(b, q, j, t, line, NQ, nt, nlines));
+        r.uv[j] = __ldg(UV + uidx(b, q, j, line, NQ, nlines));
     }
 }
 // x = hi + lo: hi = x rounded to tf32's 10 mantissa bits (half away from zero, two integer ops; the
@@ -966,8 +971,9 @@ __device__ __forceinline__ void tc_write_operand(uint32_t tah, uint32_t tal, V v
     tmem_st8(tah + 32, hi);
     tmem_st8(tal + 32, lo);
 }
-// the 15 MMAs of one M half of a blur (5 k-steps, 3 tf32 products), one thread
-__device__ __forceinline__ void tc_blur_mmas(uint32_t tb, uint32_t bm, int h) {
+// the 15 MMAs of one M half of a blur (5 k-steps, 3 tf32 products), one thread; tensor memory of NH
+// halves: D[h] at columns 32 h, A_hi[h] / A_lo[h] at 32 NH + 80 h (+ 40)
+__device__ __forceinline__ void tc_blur_mmas(uint32_t tb, uint32_t bm, int h, int NH = 2) {
     constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
     auto desc = [](uint32_t start) -> uint64_t {   // K-major, no swizzle: LBO 128 B (K), SBO 1280 B (N)
         return (uint64_t)((start >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(1280 >> 4) << 32) |
@@ -980,7 +986,7 @@ __device__ __forceinline__ void tc_blur_mmas(uint32_t tb, uint32_t bm, int h) {
             "r"(a), "l"(b), "r"(idesc), "r"(acc)
             : "memory");
     };
-    const uint32_t td = tb + 32 * h, tah = tb + 64 + 80 * h, tal = tah + 40;
+    const uint32_t td = tb + 32 * h, tah = tb + 32 * NH + 80 * h, tal = tah + 40;
 #pragma unroll
     for (int ks = 0; ks < 5; ++ks) {
         const uint64_t bh = desc(bm + ks * 256), bl = desc(bm + 4 * 1280 + ks * 256);
@@ -1008,18 +1014,23 @@ __device__ __forceinline__ void tc_wait(uint64_t *bar, uint32_t parity) {
 #endif
 }
 
-__global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant__ RecTArgs a) {
-    constexpr int D = 3;
+template <int NP>
+__global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 : 1)
+    rect_tc2_kernel(const __grid_constant__ RecTArgs a) {
+    using L = TcSmem<NP>;
+    constexpr int D = L::D, NQ = L::NQ, NH = L::NH, NT = 128 * NH;
     extern __shared__ __align__(128) float smt[];
-    float *fs = smt + TcSmem::OFF_FS;
-    float *csb = smt + TcSmem::OFF_CS;   // double-buffered: sample b in csb + (b & 1) * 2 T TP
-    float *bmat = smt + TcSmem::OFF_B;
-    float *tr = smt + TcSmem::OFF_TR;
-    float4 *pfb = reinterpret_cast<float4 *>(smt + TcSmem::OFF_PFB);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smt + TcSmem::OFF_BAR);
-    uint32_t *tbase_s = reinterpret_cast<uint32_t *>(smt + TcSmem::OFF_BAR + 4);
+    float *fs = smt + L::OFF_FS;
+    float *csb = smt + L::OFF_CS;   // double-buffered: sample b in csb + (b & 1) * 2 T TP
+    float *bmat = smt + L::OFF_B;
+    float *tr = smt + L::OFF_TR;
+    float4 *pfb = reinterpret_cast<float4 *>(smt + L::OFF_PFB);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smt + L::OFF_BAR);
+    uint32_t *tbase_s = reinterpret_cast<uint32_t *>(smt + L::OFF_BAR + 2 * NH);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int half = warp >> 2, qw = warp & 3, q = 4 * half + qw, p = q >> 1, part = q & 1;
+    const bool real_plane = q < NQ;   // padding planes of the last half: operands only, no output
+    const int qq = real_plane ? q : NQ - 1, pp = qq >> 1;   // a valid plane for their (unused) loads
     const int ntxf = a.W / T;
     const int tx = blockIdx.x % ntxf, ty = blockIdx.x / ntxf;
     const int x0 = tx * T, y0 = ty * T, H = a.H, W = a.W;
@@ -1027,11 +1038,11 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     const int G = a.g3, g = blockIdx.y;
     const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
 
-    for (int e = tid; e < D * T * T; e += 256) {   // centred f tile (reading R12)
+    for (int e = tid; e < D * T * T; e += NT) {   // centred f tile (reading R12)
         const int c = e / (T * T), i = (e / T) % T, j = e % T;
         fs[(c * T + i) * TP + j] = a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c];
     }
-    for (int e = tid; e < kRecTcB; e += 256) bmat[e] = __ldg(a.tcb + e);
+    for (int e = tid; e < kRecTcB; e += NT) bmat[e] = __ldg(a.tcb + e);
     if (tid < 4) {
         const int ax = tid >> 1, j = tid & 1;
         const RecTabs &tb = ax ? a.tv : a.th;
@@ -1040,13 +1051,12 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
         pfb[tid] = make_float4(pf.x, pf.y, pb.x, pb.y);
     }
     if (tid == 0) {
-        mbar_init(bar, 1);
-        mbar_init(bar + 1, 1);
+        for (int h = 0; h < NH; ++h) mbar_init(bar + h, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tbase_s)),
-                     "n"(kTcCols)
+                     "n"(L::COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -1056,7 +1066,7 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tb = *tbase_s;
     const uint32_t loff = (uint32_t)(qw * 32) << 16;
-    const uint32_t td = tb + 32 * half + loff, tah = tb + 64 + 80 * half + loff, tal = tah + 40;
+    const uint32_t td = tb + 32 * half + loff, tah = tb + 32 * NH + 80 * half + loff, tal = tah + 40;
     const uint32_t bm = saddr(bmat);
 
     float acc[T];
@@ -1065,8 +1075,8 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     RawP rraw, craw;
     float tn[D];
     if (s0 < s1) {
-        load_rawp(a.Eh, a.Bh, a.UVh, s0, q, tx, y0 + lane, a.ntx, a.nlh, rraw);
-        load_rawp(a.Ev, a.Bv, a.UVv, s0, q, ty, x0 + lane, a.nty, W, craw);
+        load_rawp<NQ>(a.Eh, a.Bh, a.UVh, s0, qq, tx, y0 + lane, a.ntx, a.nlh, rraw);
+        load_rawp<NQ>(a.Ev, a.Bv, a.UVv, s0, qq, ty, x0 + lane, a.nty, W, craw);
 #pragma unroll
         for (int c = 0; c < D; ++c) tn[c] = __ldg(a.t + (long long)(a.k0 + s0) * D + c);
     }
@@ -1074,7 +1084,7 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     // modulation runs while this sample's column blur is on the tensor cores
     auto modulate = [&](int b, const float (&tk)[D]) {
         float *c = csb + (b & 1) * 2 * T * TP;
-        for (int e = tid; e < T * T; e += 256) {
+        for (int e = tid; e < T * T; e += NT) {
             const int i = e / T, j = e % T;
             float th = 0.f;
 #pragma unroll
@@ -1100,19 +1110,19 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
         // part (cos / sin) and pair 0 (no f factor) are warp-uniform: one instance each, no selects
         {
             const float *hrow = cs + part * T * TP + lane * TP;
-            const float *frow = fs + ((p > 0 ? p - 1 : 0) * T + lane) * TP;
-            if (p > 0)
+            const float *frow = fs + ((pp > 0 ? pp - 1 : 0) * T + lane) * TP;
+            if (pp > 0)
                 tc_write_operand(tah, tal, [&](int m) -> float { return hrow[m] * frow[m]; }, rraw, pfb);
             else
                 tc_write_operand(tah, tal, [&](int m) -> float { return hrow[m]; }, rraw, pfb);
         }
-        if (b + 1 < s1) load_rawp(a.Eh, a.Bh, a.UVh, b + 1, q, tx, y0 + lane, a.ntx, a.nlh, rraw);
+        if (b + 1 < s1) load_rawp<NQ>(a.Eh, a.Bh, a.UVh, b + 1, qq, tx, y0 + lane, a.ntx, a.nlh, rraw);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         named_sync<128>(1 + half);   // the two M halves run as independent pipelines
         if ((tid & 127) == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            tc_blur_mmas(tb, bm, half);
+            tc_blur_mmas(tb, bm, half, NH);
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              saddr(bar + half))
                          : "memory");
@@ -1133,13 +1143,13 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
             const float *tcol = tr + warp * T * TP + lane;
             tc_write_operand(tah, tal, [&](int m) -> float { return tcol[m * TP]; }, craw, pfb + 2);
         }
-        if (b + 1 < s1) load_rawp(a.Ev, a.Bv, a.UVv, b + 1, q, ty, x0 + lane, a.nty, W, craw);
+        if (b + 1 < s1) load_rawp<NQ>(a.Ev, a.Bv, a.UVv, b + 1, qq, ty, x0 + lane, a.nty, W, craw);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         named_sync<128>(1 + half);   // the two M halves run as independent pipelines
         if ((tid & 127) == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            tc_blur_mmas(tb, bm, half);
+            tc_blur_mmas(tb, bm, half, NH);
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              saddr(bar + half))
                          : "memory");
@@ -1166,13 +1176,13 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     }
     // the pair's two planes (warps w, w + 1) summed into the output plane of pair p
     __syncthreads();
-    if (part) {
+    if (part && real_plane) {
         float *o = tr + warp * T * TP + lane;
 #pragma unroll
         for (int i = 0; i < T; ++i) o[i * TP] = acc[i];
     }
     __syncthreads();
-    if (!part) {
+    if (!part && real_plane) {
         const float *o = tr + (warp + 1) * T * TP + lane;
         const int pl = (p == 0) ? D : p - 1;
         float *dst = a.pz + ((long long)g * (D + 1) + pl) * plane + (long long)y0 * W + x0 + lane;
@@ -1185,14 +1195,16 @@ __global__ void __launch_bounds__(256, 2) rect_tc2_kernel(const __grid_constant_
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(kTcCols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(L::COLS) : "memory");
 }
 
+template <int NP>
 cudaError_t launch_tc2(const RecTArgs &a, cudaStream_t s) {
+    using L = TcSmem<NP>;
     static std::atomic<uint64_t> attr{0};
-    cudaError_t e = ensure_smem_attr(rect_tc2_kernel, TcSmem::BYTES, attr);
+    cudaError_t e = ensure_smem_attr(rect_tc2_kernel<NP>, L::BYTES, attr);
     if (e != cudaSuccess) return e;
-    rect_tc2_kernel<<<dim3((a.W / T) * (a.H / T), a.g3), 256, TcSmem::BYTES, s>>>(a);
+    rect_tc2_kernel<NP><<<dim3((a.W / T) * (a.H / T), a.g3), 128 * L::NH, L::BYTES, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1425,16 +1437,18 @@ cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
     cudaError_t e = launch_tile<NP, 0>(a, a.g1, s);
     if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.nlh, nq, s);
     if (e == cudaSuccess && a.vl != nullptr) {   // rec_impl 2: virtual-line row blur inside the column scan
-        e = (a.tc && a.vtc) ? launch_vscan_tc(a, 2 * NP, s) : launch_vscan(a, 2 * NP, s);
+        e = a.vtc ? launch_vscan_tc(a, 2 * NP, s) : launch_vscan(a, 2 * NP, s);
     } else {
         if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
         if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
     }
     if (e != cudaSuccess) return e;
-    if (NP == 4 && a.tc) {   // full tiles on the tensor cores, the rest (if any) on the FP32 path
-        if (a.W % T || a.H % T) e = launch_tile<NP, 2>(a, a.g3, s);
-        if (e == cudaSuccess && a.W >= T && a.H >= T) e = launch_tc2(a, s);
-        return e;
+    if constexpr (NP <= 8) {
+        if (a.tc) {   // full tiles on the tensor cores, the rest (if any) on the FP32 path
+            if (a.W % T || a.H % T) e = launch_tile<NP, 2>(a, a.g3, s);
+            if (e == cudaSuccess && a.W >= T && a.H >= T) e = launch_tc2<NP>(a, s);
+            return e;
+        }
     }
     return launch_tile<NP, 2>(a, a.g3, s);
 }

@@ -173,3 +173,33 @@ def test_tensor_core_pass2_equals_fp32_pass2(shape, rec_impl):
     err = np.abs(out[1] - out[0]).max() / scale
     print(f"{shape} rec_impl {rec_impl}: max |tc - fp32| / max = {err:.2e}")
     assert err <= 2e-6
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 5, 7])
+@pytest.mark.parametrize("shape", [(96, 160), (100, 150)])
+def test_tensor_core_recursion_other_channel_counts(d, shape, rec_impl):
+    """The tensor-core segment blurs for d != 3 (pass 2 in ceil(2(d+1)/4) M halves, the last one
+    padded for even d; the column scan's virtual lines for any d when W is a multiple of 32): the
+    same partial sums as the FP32 recursion to fp32 rounding (2e-6 of the largest sum), and Gate A
+    against the oracle."""
+    if rec_impl != 2 or not _IMPL["rec_tc"] or not _IMPL["rec_vtc"]:
+        pytest.skip("one fixture instance is enough")
+    Hh, Ww = shape
+    cfg = small_config(d=d, H=Hh, W=Ww, sigma_s=3.0, N=12, M=5, seed=d + Hh)
+    f_np = random_image(Hh, Ww, d, seed=d + Ww, smooth=True)
+    f = torch.from_numpy(f_np).cuda()
+    out = {}
+    for tc in (0, 1):
+        p = H.gpu_plan(cfg)
+        p.set_option("engine", 1)
+        p.set_option("rec_impl", 2)
+        p.set_option("rec_tc", tc)
+        out[tc] = p.filter_partial(f, 0, cfg.M).cpu().numpy().astype(np.float64)
+    err = np.abs(out[1] - out[0]).max() / np.abs(out[0]).max()
+    Q, a, Y = H.oracle_draws(cfg)
+    S_o, P_o, Z_o = native.mcsf_full(f_np, Q, a, cfg.N, Y, cfg.sigma_s, spatial="deriche")
+    p = _rec_plan(cfg)
+    res = H.gates(cfg, *H.gpu_run(p, f_np), S_o, P_o, Z_o)
+    print(f"d {d} {shape}: max |tc - fp32| / max = {err:.2e}, {res}")
+    assert err <= 2e-6
+    H.assert_gates(res)
