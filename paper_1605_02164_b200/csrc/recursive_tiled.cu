@@ -901,7 +901,7 @@ struct TcSmem {
     static constexpr size_t BYTES = sizeof(float) * (OFF_BAR + 2 * NH + 2);
     static constexpr int COLS = NH <= 2 ? 256 : 512;          // tensor memory: 112 columns per half
 };
-constexpr int kTcCols = 256;   // D[2] (32 each), A_hi[2] / A_lo[2] (40 each) at 64 + 80 h (+ 40)
+constexpr int kTcCols = 256;   // two M halves (the column scan): D[2] (32 each), A_hi[2] / A_lo[2] (40 each) at 64 + 80 h (+ 40)
 
 struct RawP {   // one plane's entering-state inputs: [pole j]
     float2 e[2], bb[2];
