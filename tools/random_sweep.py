@@ -22,13 +22,18 @@ from tests.gpu import helpers as H  # noqa: E402
 from workloads.configs import random_image, small_config  # noqa: E402
 
 
+REC_FRAC, W32 = 0.25, 0.0   # --rec-frac, --w32
+
+
 def case(rng, i):
     d = int(rng.choice([1, 2, 3, 3, 3, 4, 5, 8]))
     Hh, W = int(rng.integers(1, 160)), int(rng.integers(1, 200))
+    if rng.random() < W32:   # widths the column scan's tensor-core path takes
+        W = 32 * int(rng.integers(1, 7))
     s = float(rng.choice([0.5, 1.0, 2.2, 3.7, 5.0, 8.0, 12.0, 16.0]))
     N = int(rng.choice([4, 10, 20, 40]))
     M = int(rng.integers(1, 24))
-    engine = int(rng.random() < 0.25)
+    engine = int(rng.random() < REC_FRAC)
     spatial = "gaussian" if engine else str(rng.choice(["gaussian", "gaussian", "box", "hat"]))
     sampler = int(rng.random() < 0.3)
     sched = str(rng.choice(["auto", "forced", "persistent"]))
@@ -85,7 +90,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=200)
     ap.add_argument("--seed", type=int, default=9)
+    ap.add_argument("--rec-frac", type=float, default=0.25, help="share of recursive-engine cases")
+    ap.add_argument("--w32", type=float, default=0.0, help="share of widths rounded to a multiple of 32")
     args = ap.parse_args()
+    global REC_FRAC, W32
+    REC_FRAC, W32 = args.rec_frac, args.w32
     rng = np.random.default_rng(args.seed)
     n_ok = n_fail = n_skip = 0
     for i in range(args.n):
