@@ -1031,25 +1031,14 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
     const int half = warp >> 2, qw = warp & 3, q = 4 * half + qw, p = q >> 1, part = q & 1;
     const bool real_plane = q < NQ;   // padding planes of the last half: operands only, no output
     const int qq = real_plane ? q : NQ - 1, pp = qq >> 1;   // a valid plane for their (unused) loads
-    const int ntxf = a.W / T;
-    const int tx = blockIdx.x % ntxf, ty = blockIdx.x / ntxf;
-    const int x0 = tx * T, y0 = ty * T, H = a.H, W = a.W;
+    const int ntxf = a.W / T, ntiles = ntxf * (a.H / T);
+    const int H = a.H, W = a.W;
     const long long plane = (long long)H * W;
     const int G = a.g3, g = blockIdx.y;
     const int s0 = (int)((long long)a.ns * g / G), s1 = (int)((long long)a.ns * (g + 1) / G);
 
-    for (int e = tid; e < D * T * T; e += NT) {   // centred f tile (reading R12)
-        const int c = e / (T * T), i = (e / T) % T, j = e % T;
-        fs[(c * T + i) * TP + j] = a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c];
-    }
+    // persistent CTA: the matrix, the barriers and the tensor memory are set up once for all its tiles
     for (int e = tid; e < kRecTcB; e += NT) bmat[e] = __ldg(a.tcb + e);
-    if (tid < 4) {
-        const int ax = tid >> 1, j = tid & 1;
-        const RecTabs &tb = ax ? a.tv : a.th;
-        const int t = ax ? ty : tx, nt = ax ? a.nty : a.ntx;
-        const float2 pf = tb.pf[j * nt + t], pb = tb.pb[j * nt + t];
-        pfb[tid] = make_float4(pf.x, pf.y, pb.x, pb.y);
-    }
     if (tid == 0) {
         for (int h = 0; h < NH; ++h) mbar_init(bar + h, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1068,6 +1057,23 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
     const uint32_t loff = (uint32_t)(qw * 32) << 16;
     const uint32_t td = tb + 32 * half + loff, tah = tb + 32 * NH + 80 * half + loff, tal = tah + 40;
     const uint32_t bm = saddr(bmat);
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int tx = tile % ntxf, ty = tile / ntxf;
+    const int x0 = tx * T, y0 = ty * T;
+    __syncthreads();   // the previous tile is done with fs, cs, tr and pfb
+    for (int e = tid; e < D * T * T; e += NT) {   // centred f tile (reading R12)
+        const int c = e / (T * T), i = (e / T) % T, j = e % T;
+        fs[(c * T + i) * TP + j] = a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c];
+    }
+    if (tid < 4) {
+        const int ax = tid >> 1, j = tid & 1;
+        const RecTabs &tbl = ax ? a.tv : a.th;
+        const int t = ax ? ty : tx, nt = ax ? a.nty : a.ntx;
+        const float2 pf = tbl.pf[j * nt + t], pb = tbl.pb[j * nt + t];
+        pfb[tid] = make_float4(pf.x, pf.y, pb.x, pb.y);
+    }
+    __syncthreads();
 
     float acc[T];
 #pragma unroll
@@ -1103,7 +1109,6 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
         }
     }
     __syncthreads();
-    uint32_t phase = 0;
     for (int b = s0; b < s1; ++b) {
         const float *cs = csb + (b & 1) * 2 * T * TP;
         // row operand of line (q, y = lane): the pair's modulated plane (Alg. 1) + row states;
@@ -1192,6 +1197,7 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
             dst[(long long)i * W] = a.first ? v : dst[(long long)i * W] + v;
         }
     }
+    }   // tiles
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
@@ -1204,7 +1210,16 @@ cudaError_t launch_tc2(const RecTArgs &a, cudaStream_t s) {
     static std::atomic<uint64_t> attr{0};
     cudaError_t e = ensure_smem_attr(rect_tc2_kernel<NP>, L::BYTES, attr);
     if (e != cudaSuccess) return e;
-    rect_tc2_kernel<NP><<<dim3((a.W / T) * (a.H / T), a.g3), 128 * L::NH, L::BYTES, s>>>(a);
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // persistent: as many CTAs as fit (tensor memory: two per SM up to two M halves, else one)
+    const int ntiles = (a.W / T) * (a.H / T);
+    const int ctas = std::min(ntiles, nsm * (L::NH <= 2 ? 2 : 1));
+    rect_tc2_kernel<NP><<<dim3(ctas, a.g3), 128 * L::NH, L::BYTES, s>>>(a);
     return cudaGetLastError();
 }
 
