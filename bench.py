@@ -56,6 +56,9 @@ def parse(argv=None):
                     help="engine 1, d = 3: 1 = pass 2's tile blurs on the tensor cores (tcgen05 tf32 x3, the default), 0 = FP32")
     ap.add_argument("--rec-vtc", type=int, default=-1,
                     help="engine 1 with --rec-tc 1: 1 = the column scan's virtual-line blurs on the tensor cores too (default)")
+    ap.add_argument("--rec-overlap", type=int, default=-1,
+                    help="engine 1 tiled: 1 = batch k+1's pass 0 beside batch k's scans (aux stream, high priority), "
+                         "2 = same at default priority, 0 = one stream")
     ap.add_argument("--persistent", type=int, default=-1,
                     help="v6 kernel schedule: 1 auto (library default), 0 classic grid, 2 persistent")
     ap.add_argument("--rec-store", type=int, default=-1,
@@ -343,6 +346,8 @@ def run_ours(args, cfg):
         plan.set_option("rec_vtc", args.rec_vtc)
     if args.rec_store >= 0:
         plan.set_option("rec_store", args.rec_store)
+    if args.rec_overlap >= 0:
+        plan.set_option("rec_overlap", args.rec_overlap)
     if args.persistent >= 0:
         plan.set_option("persistent", args.persistent)
     plan.sample_freqs()

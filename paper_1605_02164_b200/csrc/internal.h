@@ -166,7 +166,8 @@ struct RecTArgs {
     float4 zpq[kRecT];    // the same regrouped (Re z_0^m, Re z_1^m, Im z_0^m, Im z_1^m): both poles of one
                           // real line in one FFMA2 (rec_impl 2's virtual-line summaries)
 };
-cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s);
+constexpr int kRecStageP0 = 1, kRecStageScan = 2, kRecStageP2 = 4, kRecStageAll = 7;
+cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s, int stages = kRecStageAll);
 
 // Error-vs-T sweep (sweep.cu): fold partial groups into running (P', Z), S = P'/Z + mu,
 // accumulate sum (ref - S)^2 into *out (double).
@@ -229,6 +230,12 @@ struct bf_vec_plan_s {
     int rec_impl = 2;          // recursive engine: 0 staged (row / column passes via HBM), 1 tiled, 2 tiled + virtual lines
     int rec_tc = 1;            // tiled engine: 1 = pass 2's tile blurs (d <= 7) as block-Toeplitz GEMMs on the tensor cores
     int rec_vtc = 1;           // with rec_tc: the column scan's virtual-line segment blurs on the tensor cores too
+    int rec_overlap = 0;       // tiled engine, > 1 batch: batch k + 1's pass 0 (FP32 pipe) runs beside batch k's
+                               // scans (HBM) on a second stream, two scratch sets; 1 = that stream at high
+                               // priority, 2 = at default priority
+    cudaStream_t rec_aux = nullptr;
+    int rec_aux_prio = 0;      // the rec_overlap mode rec_aux was created for
+    cudaEvent_t rec_ev[2] = {nullptr, nullptr};   // fork (main -> aux), join (aux -> main)
     float2 *drtab = nullptr;   // tiled recursive engine: pole-power tables of both axes
     size_t drtab_n = 0;
     int sampler = 0;           // 0 iid binomial draws (reading R9), 1 stratified (reading R17)

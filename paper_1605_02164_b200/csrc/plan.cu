@@ -829,30 +829,32 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     const size_t rb_per = (p->rec_store && !vlines) ? sizeof(float) * (size_t)NQ * px : 0;   // stored row blur
     const size_t vl_per = vlines ? sizeof(float) * (size_t)NQ * nty * 8 * p->W : 0;
     const size_t per = sizeof(float2) * 2 * (sum_h + sum_v) + sizeof(float4) * (uv_h + uv_v) + rb_per + vl_per;
-    int nb = 1, g = 1;
+    int nb = 1, g = 1, sets = 1;
     bf_status_t st = BF_OK;
     for (int attempt = 0; attempt < 2; ++attempt) {
         const size_t free_b = free_memory(p);
         // batch: up to 256 samples within 40 % of the free memory, but no more than 16 samples or
         // 4 GiB of summaries (whichever allows more) -- a larger batch only saves launches (5 per batch)
         const double cap = std::max(16.0, 4.0 * 1024 * 1024 * 1024 / (double)per);
-        nb = (int)std::max(1.0, std::min({256.0, 0.4 * (double)free_b / (double)per, cap}));
+        const double sets_max = p->rec_overlap ? 2.0 : 1.0;   // overlap: two scratch sets in flight
+        nb = (int)std::max(1.0, std::min({256.0, 0.4 * (double)free_b / (sets_max * (double)per), cap}));
         if (p->force_batch > 0) nb = p->force_batch;
         nb = std::min(nb, ns);
+        sets = (p->rec_overlap && ns > nb) ? 2 : 1;
         // sample groups: enough CTAs for ~8 per SM where the tile count alone does not give them
         const long long want = 8LL * sm_count();
         g = (int)std::min<long long>(nb, std::max<long long>(1, (want + tiles - 1) / tiles));
         st = BF_OK;
-        if (p->drec_bytes < per * nb) {
+        if (p->drec_bytes < per * nb * sets) {
             cudaFree(p->drec);
             p->drec = nullptr;
             p->drec_bytes = 0;
-            if (cudaMalloc(&p->drec, per * nb) != cudaSuccess) {
+            if (cudaMalloc(&p->drec, per * nb * sets) != cudaSuccess) {
                 p->drec = nullptr;
                 st = BF_E_CUDA;
             } else {
                 p->gen += 1;   // a captured filter graph holds the old pointer: re-capture
-                p->drec_bytes = per * nb;
+                p->drec_bytes = per * nb * sets;
             }
         }
         if (st == BF_OK) st = ensure_pz(p, sizeof(float) * (size_t)g * (p->d + 1) * px);
@@ -876,16 +878,20 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     a.nty = nty;
     a.g1 = g;
     a.g3 = g;
-    float2 *base = reinterpret_cast<float2 *>(p->drec);
-    a.Eh = base;
-    a.Bh = a.Eh + (size_t)nb * sum_h;
-    a.Ev = a.Bh + (size_t)nb * sum_h;
-    a.Bv = a.Ev + (size_t)nb * sum_v;
-    a.UVh = reinterpret_cast<float4 *>(a.Bv + (size_t)nb * sum_v);
-    a.UVv = a.UVh + (size_t)nb * uv_h;
-    a.rbg = rb_per ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
+    // scratch set k (of `sets`): summaries, line states, stored row blur / virtual-line values
+    auto set_scratch = [&](RecTArgs &x, int k) {
+        float2 *base = reinterpret_cast<float2 *>(reinterpret_cast<char *>(p->drec) + per * nb * k);
+        x.Eh = base;
+        x.Bh = x.Eh + (size_t)nb * sum_h;
+        x.Ev = x.Bh + (size_t)nb * sum_h;
+        x.Bv = x.Ev + (size_t)nb * sum_v;
+        x.UVh = reinterpret_cast<float4 *>(x.Bv + (size_t)nb * sum_v);
+        x.UVv = x.UVh + (size_t)nb * uv_h;
+        x.rbg = rb_per ? reinterpret_cast<float *>(x.UVv + (size_t)nb * uv_v) : nullptr;
+        x.vl = vlines ? reinterpret_cast<float *>(x.UVv + (size_t)nb * uv_v) : nullptr;
+    };
+    set_scratch(a, 0);
     a.nlh = nlh;
-    a.vl = vlines ? reinterpret_cast<float *>(a.UVv + (size_t)nb * uv_v) : nullptr;
     a.tcb = reinterpret_cast<const float *>(a.th.zp + kRecT);
     a.tc = (p->rec_tc && p->d <= 7) ? 1 : 0;   // up to four M halves (16 planes) in tensor memory
     a.vtc = (p->rec_vtc && p->rec_tc && p->W % kRecT == 0) ? 1 : 0;
@@ -908,11 +914,46 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
             if (!p->ev[slot][j]) BF_CUDA(cudaEventCreate(&p->ev[slot][j]));
         BF_CUDA(cudaEventRecord(p->ev[slot][0], s));
     }
-    for (int kb = k0; kb < k1; kb += nb) {
-        a.k0 = kb;
-        a.ns = std::min(nb, k1 - kb);
-        a.first = (kb == k0) ? 1 : 0;
-        BF_CUDA(launch_recursive_tiled(a, s));
+    auto batch = [&](int i) {   // batch i's arguments: samples [k0 + i nb, ...), scratch set i % sets
+        RecTArgs x = a;
+        x.k0 = k0 + i * nb;
+        x.ns = std::min(nb, k1 - x.k0);
+        x.first = (i == 0) ? 1 : 0;
+        set_scratch(x, i % sets);
+        return x;
+    };
+    const int nbat = (ns + nb - 1) / nb;
+    if (sets == 1) {
+        for (int i = 0; i < nbat; ++i) BF_CUDA(launch_recursive_tiled(batch(i), s));
+    } else {
+        // overlap (option rec_overlap): batch i's scans on the auxiliary stream while batch i + 1's
+        // pass 0 runs on s; pass 2 of batch i (which accumulates into the shared partial planes) on s
+        // after both. Set (i + 1) % 2 is free when pass 0 of batch i + 1 starts: pass 2 of batch i - 1,
+        // its last reader, precedes it on s.
+        if (!p->rec_aux || p->rec_aux_prio != p->rec_overlap) {
+            if (p->rec_aux) {
+                cudaStreamSynchronize(p->rec_aux);
+                cudaStreamDestroy(p->rec_aux);
+                p->rec_aux = nullptr;
+            }
+            int lo = 0, hi = 0;
+            BF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            BF_CUDA(cudaStreamCreateWithPriority(&p->rec_aux, cudaStreamNonBlocking, p->rec_overlap == 1 ? hi : lo));
+            p->rec_aux_prio = p->rec_overlap;
+        }
+        for (int j = 0; j < 2; ++j)
+            if (!p->rec_ev[j]) BF_CUDA(cudaEventCreateWithFlags(&p->rec_ev[j], cudaEventDisableTiming));
+        BF_CUDA(launch_recursive_tiled(batch(0), s, kRecStageP0));
+        for (int i = 0; i < nbat; ++i) {
+            const RecTArgs x = batch(i);
+            BF_CUDA(cudaEventRecord(p->rec_ev[0], s));
+            BF_CUDA(cudaStreamWaitEvent(p->rec_aux, p->rec_ev[0], 0));
+            BF_CUDA(launch_recursive_tiled(x, p->rec_aux, kRecStageScan));
+            BF_CUDA(cudaEventRecord(p->rec_ev[1], p->rec_aux));
+            if (i + 1 < nbat) BF_CUDA(launch_recursive_tiled(batch(i + 1), s, kRecStageP0));
+            BF_CUDA(cudaStreamWaitEvent(s, p->rec_ev[1], 0));
+            BF_CUDA(launch_recursive_tiled(x, s, kRecStageP2));
+        }
     }
     if (slot >= 0) {
         BF_CUDA(cudaEventRecord(p->ev[slot][1], s));
@@ -1071,6 +1112,12 @@ void bf_vec_plan_destroy(bf_vec_plan_t p) {
             for (cudaEvent_t e : {p->ev_in[i], p->ev_comp[i], p->ev_out[i]})
                 if (e) cudaEventDestroy(e);
         }
+        if (p->rec_aux) {
+            cudaStreamSynchronize(p->rec_aux);
+            cudaStreamDestroy(p->rec_aux);
+        }
+        for (cudaEvent_t e : p->rec_ev)
+            if (e) cudaEventDestroy(e);
         if (p->copy_in) cudaStreamDestroy(p->copy_in);
         if (p->copy_out) cudaStreamDestroy(p->copy_out);
         for (auto &pair : p->ev)
@@ -1681,6 +1728,11 @@ bf_status_t bf_vec_set_option(bf_vec_plan_t p, const char *name, double v) {
         p->sampler = (int)v;   // takes effect at the next bf_vec_sample_freqs
         return BF_OK;
     }
+    if (!std::strcmp(name, "rec_overlap")) {   // A/B: batch k + 1's pass 0 beside batch k's scans
+        if (v != 0.0 && v != 1.0 && v != 2.0) return BF_E_ARG;
+        p->rec_overlap = (int)v;
+        return BF_OK;
+    }
     if (!std::strcmp(name, "rec_vtc")) {   // A/B: the column scan's virtual-line blurs on the tensor cores
         if (v != 0.0 && v != 1.0) return BF_E_ARG;
         p->rec_vtc = (int)v;
@@ -1738,7 +1790,7 @@ bf_status_t bf_vec_plan_info(bf_vec_plan_t p, const char *name, long long *value
         {"launches_per_filter", p->last_launches}, {"smem_bytes", (long long)k.smem},
         {"threads", k.threads}, {"kernel_D", k.D}, {"kernel_R", k.R}, {"regs", k.regs},
         {"occupancy", k.occupancy}, {"alias", p->alias ? 1 : 0}, {"variant", k.variant},
-        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"rec_tc", p->rec_tc}, {"rec_vtc", p->rec_vtc}, {"rec_store", p->rec_store}, {"persistent", p->persistent}, {"last_persistent", p->last_persistent}, {"sampler", p->sampler}, {"colorspace", p->lab},
+        {"spatial_kernel", p->spatial}, {"graph", p->use_graph ? 1 : 0}, {"graph_ready", p->gexec ? 1 : 0}, {"engine", p->engine}, {"rec_batch", p->last_batch}, {"rec_impl", p->rec_impl}, {"rec_tc", p->rec_tc}, {"rec_vtc", p->rec_vtc}, {"rec_overlap", p->rec_overlap}, {"rec_store", p->rec_store}, {"persistent", p->persistent}, {"last_persistent", p->last_persistent}, {"sampler", p->sampler}, {"colorspace", p->lab},
         {"fir_supported", p->r <= kMaxR ? 1 : 0},
     };
     for (auto &e : tab)

@@ -1446,18 +1446,23 @@ cudaError_t launch_scan(float2 *E, float2 *B, float4 *UV, const RecTabs &tb, con
     return cudaGetLastError();
 }
 
+// stages (bit mask, DESIGN.md §11 "overlap"): kRecStageP0 = pass 0 (summaries), kRecStageScan = the
+// scans (and pass 1 of rec_impl 1), kRecStageP2 = pass 2; all three in order by default
 template <int NP>
-cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
+cudaError_t launch_np(const RecTArgs &a, cudaStream_t s, int stages) {
     const long long nq = (long long)a.ns * 2 * NP;
-    cudaError_t e = launch_tile<NP, 0>(a, a.g1, s);
-    if (e == cudaSuccess) e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.nlh, nq, s);
-    if (e == cudaSuccess && a.vl != nullptr) {   // rec_impl 2: virtual-line row blur inside the column scan
-        e = a.vtc ? launch_vscan_tc(a, 2 * NP, s) : launch_vscan(a, 2 * NP, s);
-    } else {
-        if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
-        if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
+    cudaError_t e = cudaSuccess;
+    if (stages & kRecStageP0) e = launch_tile<NP, 0>(a, a.g1, s);
+    if (e == cudaSuccess && (stages & kRecStageScan)) {
+        e = launch_scan(a.Eh, a.Bh, a.UVh, a.th, a.row, a.ntx, a.nlh, nq, s);
+        if (e == cudaSuccess && a.vl != nullptr) {   // rec_impl 2: virtual-line row blur inside the column scan
+            e = a.vtc ? launch_vscan_tc(a, 2 * NP, s) : launch_vscan(a, 2 * NP, s);
+        } else {
+            if (e == cudaSuccess) e = launch_tile<NP, 1>(a, a.g1, s);
+            if (e == cudaSuccess) e = launch_scan(a.Ev, a.Bv, a.UVv, a.tv, a.col, a.nty, a.W, nq, s);
+        }
     }
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess || !(stages & kRecStageP2)) return e;
     if constexpr (NP <= 8) {
         if (a.tc) {   // full tiles on the tensor cores, the rest (if any) on the FP32 path
             if (a.W % T || a.H % T) e = launch_tile<NP, 2>(a, a.g3, s);
@@ -1470,16 +1475,16 @@ cudaError_t launch_np(const RecTArgs &a, cudaStream_t s) {
 
 }  // namespace
 
-cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s) {
+cudaError_t launch_recursive_tiled(const RecTArgs &a, cudaStream_t s, int stages) {
     switch (a.d) {
-        case 1: return launch_np<2>(a, s);
-        case 2: return launch_np<3>(a, s);
-        case 3: return launch_np<4>(a, s);
-        case 4: return launch_np<5>(a, s);
-        case 5: return launch_np<6>(a, s);
-        case 6: return launch_np<7>(a, s);
-        case 7: return launch_np<8>(a, s);
-        case 8: return launch_np<9>(a, s);
+        case 1: return launch_np<2>(a, s, stages);
+        case 2: return launch_np<3>(a, s, stages);
+        case 3: return launch_np<4>(a, s, stages);
+        case 4: return launch_np<5>(a, s, stages);
+        case 5: return launch_np<6>(a, s, stages);
+        case 6: return launch_np<7>(a, s, stages);
+        case 7: return launch_np<8>(a, s, stages);
+        case 8: return launch_np<9>(a, s, stages);
     }
     return cudaErrorInvalidValue;
 }

@@ -203,3 +203,34 @@ def test_tensor_core_recursion_other_channel_counts(d, shape, rec_impl):
     print(f"d {d} {shape}: max |tc - fp32| / max = {err:.2e}, {res}")
     assert err <= 2e-6
     H.assert_gates(res)
+
+
+@pytest.mark.parametrize("overlap", [1, 2])
+@pytest.mark.parametrize("shape", [(96, 128, 3, 2.0, 20, 11, 12), (131, 77, 3, 5.0, 30, 17, 13)],
+                         ids=["full_tiles", "ragged"])
+def test_overlap_schedule_bitwise(overlap, shape):
+    """Option "rec_overlap": batch k + 1's pass 0 on the plan's stream while batch
+    k's scans run on an auxiliary stream, two scratch sets. Every kernel does the same arithmetic on
+    the same inputs, so the output must be bitwise that of the one-stream schedule, over several
+    batches (incl. a short last one), through both the eager and the graph-replayed call; and it
+    passes the gates against the oracle."""
+    if _IMPL["rec_impl"] == 0:
+        pytest.skip("the staged engine has one schedule")
+    cfg = _edge_cfg(shape + ("full",))
+    f = random_image(cfg.H, cfg.W, cfg.d, seed=cfg.seed, smooth=True)
+    outs = {}
+    for ov in (0, overlap):
+        p = _rec_plan(cfg, batch=4)   # 17 or 11 samples: 3-5 batches, the last one short
+        p.set_option("rec_overlap", ov)
+        ft = torch.from_numpy(np.ascontiguousarray(f)).cuda()
+        out = torch.empty((cfg.d, cfg.H, cfg.W), dtype=torch.float32, device="cuda")
+        runs = [p.filter(ft, out).cpu().numpy() for _ in range(3)]   # eager, capture, replay
+        for r in runs[1:]:
+            assert np.array_equal(r, runs[0])
+        outs[ov] = (runs[0], H.gpu_run(p, f))
+    assert np.array_equal(outs[0][0], outs[overlap][0])
+    for a, b in zip(outs[0][1], outs[overlap][1]):
+        assert np.array_equal(a, b)
+    Q, a, Y = H.oracle_draws(cfg)
+    S_o, P_o, Z_o = native.mcsf_full(f, Q, a, cfg.N, Y, cfg.sigma_s, spatial="deriche")
+    H.assert_gates(H.gates(cfg, *outs[overlap][1], S_o, P_o, Z_o))

@@ -24,6 +24,7 @@ ap.add_argument("--engine", type=int, default=0)
 ap.add_argument("--sigma", type=float, default=0.0, help="override sigma_s (recursive engine sweeps)")
 ap.add_argument("--rec-impl", type=int, default=-1, help="recursive engine: 0 staged, 1 tiled, 2 virtual lines (default)")
 ap.add_argument("--rec-tc", type=int, default=-1, help="recursive engine, d = 3: 1 tensor-core pass 2")
+ap.add_argument("--rec-overlap", type=int, default=-1, help="recursive engine: pass 0 / scan overlap mode")
 ap.add_argument("--rec-vtc", type=int, default=-1, help="recursive engine: 1 tensor-core virtual-line blurs")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
@@ -50,6 +51,8 @@ if a.rec_tc >= 0:
     p.set_option('rec_tc', a.rec_tc)
 if a.rec_vtc >= 0:
     p.set_option('rec_vtc', a.rec_vtc)
+if a.rec_overlap >= 0:
+    p.set_option('rec_overlap', a.rec_overlap)
 slab = torch.from_numpy(make_image_rows(cfg, s0, s1)).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for i in range(a.reps):
