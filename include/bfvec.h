@@ -334,6 +334,12 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 recursion everywhere. Results equal to fp32 rounding.
  *   "rec_vtc"     with rec_tc = 1, rec_impl 2 and W a multiple of 32 (any d): 1 (default) the
  *                 column scan's virtual-line segment blurs run as the same tensor-core product.
+ *   "rec_overlap" engine 1, tiled, more than one batch: 1 batch k + 1's pass 0 (FP32 pipe) runs on
+ *                 the call's stream while batch k's scans (HBM) run on a plan-owned auxiliary
+ *                 stream at high priority, forked from and joined back into the call's stream
+ *                 (graph-capturable); two scratch sets in flight instead of one. 2: the same with
+ *                 the auxiliary stream at default priority. 0: one stream. Output bitwise equal
+ *                 in every mode (the same kernels on the same inputs).
  *   "rec_store"   engine 1, rec_impl 1 (ignored by 2): 1 pass 1 stores its exact row blur (2(d+1) fp32 planes per
  *                 sample in flight) and pass 2 reads it instead of recomputing it; 0 (default)
  *                 recompute (measured 2 % faster on config 5)
