@@ -59,6 +59,7 @@ def parse(argv=None):
     ap.add_argument("--rec-overlap", type=int, default=-1,
                     help="engine 1 tiled: 1 = batch k+1's pass 0 beside batch k's scans (aux stream, high priority), "
                          "2 = same at default priority, 0 = one stream")
+    ap.add_argument("--rec-batch", type=int, default=-1, help="engine 1: samples per batch (0 = auto, the default)")
     ap.add_argument("--persistent", type=int, default=-1,
                     help="v6 kernel schedule: 1 auto (library default), 0 classic grid, 2 persistent")
     ap.add_argument("--rec-store", type=int, default=-1,
@@ -348,6 +349,8 @@ def run_ours(args, cfg):
         plan.set_option("rec_store", args.rec_store)
     if args.rec_overlap >= 0:
         plan.set_option("rec_overlap", args.rec_overlap)
+    if args.rec_batch >= 0:
+        plan.set_option("rec_batch", args.rec_batch)
     if args.persistent >= 0:
         plan.set_option("persistent", args.persistent)
     plan.sample_freqs()
