@@ -814,6 +814,10 @@ bf_status_t ensure_rec_tabs(bf_vec_plan_t p, RecTabs *th, RecTabs *tv) {
     return BF_OK;
 }
 
+#ifndef BFVEC_REC_BATCH_CAP
+#define BFVEC_REC_BATCH_CAP 48
+#endif
+constexpr int kRecBatchCap = BFVEC_REC_BATCH_CAP;
 bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1, cudaStream_t s, int *groups_out) {
     const int ns = k1 - k0;
     const int NQ = 2 * (p->d + 1);
@@ -833,9 +837,11 @@ bf_status_t run_recursive_tiled(bf_vec_plan_t p, const float *f, int k0, int k1,
     bf_status_t st = BF_OK;
     for (int attempt = 0; attempt < 2; ++attempt) {
         const size_t free_b = free_memory(p);
-        // batch: up to 256 samples within 40 % of the free memory, but no more than 16 samples or
-        // 4 GiB of summaries (whichever allows more) -- a larger batch only saves launches (5 per batch)
-        const double cap = std::max(16.0, 4.0 * 1024 * 1024 * 1024 / (double)per);
+        // batch: up to 256 samples within 40 % of the free memory, but no more than kRecBatchCap samples
+        // or 4 GiB of summaries (whichever allows more). Each batch costs ~2.5 ms beyond its samples'
+        // work on config 5 (launch drains, the partial-plane read-modify-write): 16 -> 32 -> 48 samples
+        // per batch measured 3.27 -> 3.42 -> 3.46e10 pixel*samples/s
+        const double cap = std::max((double)kRecBatchCap, 4.0 * 1024 * 1024 * 1024 / (double)per);
         const double sets_max = p->rec_overlap ? 2.0 : 1.0;   // overlap: two scratch sets in flight
         nb = (int)std::max(1.0, std::min({256.0, 0.4 * (double)free_b / (sets_max * (double)per), cap}));
         if (p->force_batch > 0) nb = p->force_batch;

@@ -25,6 +25,7 @@ ap.add_argument("--sigma", type=float, default=0.0, help="override sigma_s (recu
 ap.add_argument("--rec-impl", type=int, default=-1, help="recursive engine: 0 staged, 1 tiled, 2 virtual lines (default)")
 ap.add_argument("--rec-tc", type=int, default=-1, help="recursive engine, d = 3: 1 tensor-core pass 2")
 ap.add_argument("--rec-overlap", type=int, default=-1, help="recursive engine: pass 0 / scan overlap mode")
+ap.add_argument("--rec-batch", type=int, default=-1, help="recursive engine: samples per batch (0 auto)")
 ap.add_argument("--rec-vtc", type=int, default=-1, help="recursive engine: 1 tensor-core virtual-line blurs")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
@@ -53,6 +54,8 @@ if a.rec_vtc >= 0:
     p.set_option('rec_vtc', a.rec_vtc)
 if a.rec_overlap >= 0:
     p.set_option('rec_overlap', a.rec_overlap)
+if a.rec_batch >= 0:
+    p.set_option('rec_batch', a.rec_batch)
 slab = torch.from_numpy(make_image_rows(cfg, s0, s1)).cuda()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 for i in range(a.reps):
@@ -62,4 +65,4 @@ for i in range(a.reps):
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1])
     print(f"rep {i}: {ms:.3f} ms  {rows * cfg.W * M / ms * 1e3:.3e} px*samples/s  "
-          f"tile_rows={p.info('tile_rows')} groups={p.info('groups')} ctas={p.info('ctas')}")
+          f"tile_rows={p.info('tile_rows')} groups={p.info('groups')} ctas={p.info('ctas')} rec_batch={p.info('rec_batch')}")
