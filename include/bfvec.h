@@ -344,7 +344,7 @@ bf_status_t bf_vec_diag(bf_vec_plan_t plan, float *z_min, long long *n_small_z);
  *                 sample in flight) and pass 2 reads it instead of recomputing it; 0 (default)
  *                 recompute (measured 2 % faster on config 5)
  *   "rec_batch"   engine 1: samples per batch (0 = auto: at most 256 and 40 % of the free
- *                 device memory, and for the tiled engine at most max(16 samples, 4 GiB of
+ *                 device memory, and for the tiled engine at most max(48 samples, 4 GiB of
  *                 summaries); each sample in flight holds, staged, 5 (d+1) fp32 planes of H x W
  *                 scratch, tiled, 16 (d+1) fp32 values per 32 pixels of each axis' lines)
  *   "spatial_kernel" separable spatial taps on the window [-r, r], r = ceil(3 sigma_s):
