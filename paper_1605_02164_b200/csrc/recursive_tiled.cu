@@ -889,14 +889,33 @@ cudaError_t launch_vscan(const RecTArgs &a, int NQ, cudaStream_t s) {
 // the result, transpose the row blur through shared memory for the column operand, and fold the
 // column blur into Re[conj(H) blur] in registers (Alg. 1). Same output as pass 2.
 // NP pairs -> NQ = 2 NP planes in NH = ceil(NQ / 4) M halves of 4 planes (the last one padded)
+// pitch of pass 2's transpose rows: 36 floats, written as float4 (8 per row; each quarter-warp phase
+// hits 8 distinct 4-bank groups) and read down a column (bank 4 m + lane: conflict-free); A/B
+// BFVEC_TC_TR33: scalar stores at pitch 33
+#ifdef BFVEC_TC_TR33
+constexpr int TRP = T + 1;
+#else
+constexpr int TRP = T + 4;
+#endif
+// pitch of pass 2's f tile and (cos, sin) planes: 36, the row operand read as float4 (column reads
+// stay conflict-free: bank 4 i + lane); A/B BFVEC_TC_ROW33: pitch 33, scalar row reads. Measured with
+// the pitch-36 transposes: pass 2 14.51 -> 14.29 -> 14.23 ms per 16 config-5 samples (r2_84, r2_85)
+#ifndef BFVEC_TC_ROW33
+#define BFVEC_TC_ROWV4
+#endif
+#ifdef BFVEC_TC_ROWV4
+constexpr int CP = T + 4;
+#else
+constexpr int CP = T + 1;
+#endif
 template <int NP>
 struct TcSmem {
     static constexpr int D = NP - 1, NQ = 2 * NP, NH = (NQ + 3) / 4, WARPS = 4 * NH;
-    static constexpr int OFF_FS = 0;                          // fs[D][T][TP]
-    static constexpr int OFF_CS = D * T * TP;                 // cs[2 samples][2][T][TP]: cos plane, sin plane
-    static constexpr int OFF_B = OFF_CS + 4 * T * TP;         // B: [hi; lo] canonical layout, 16 B aligned
-    static constexpr int OFF_TR = OFF_B + kRecTcB;            // transposes [WARPS][T][TP]
-    static constexpr int OFF_PFB = OFF_TR + WARPS * T * TP;   // pfb[2 axes][2 poles] float4
+    static constexpr int OFF_FS = 0;                          // fs[D][T][CP]
+    static constexpr int OFF_CS = D * T * CP;                 // cs[2 samples][2][T][CP]: cos plane, sin plane
+    static constexpr int OFF_B = OFF_CS + 4 * T * CP;         // B: [hi; lo] canonical layout, 16 B aligned
+    static constexpr int OFF_TR = OFF_B + kRecTcB;            // transposes [WARPS][T][TRP], 16 B aligned
+    static constexpr int OFF_PFB = OFF_TR + WARPS * T * TRP;  // pfb[2 axes][2 poles] float4
     static constexpr int OFF_BAR = OFF_PFB + 16;              // mbarriers [NH], TMEM base
     static constexpr size_t BYTES = sizeof(float) * (OFF_BAR + 2 * NH + 2);
     static constexpr int COLS = NH <= 2 ? 256 : 512;          // tensor memory: 112 columns per half
@@ -1021,7 +1040,7 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
     constexpr int D = L::D, NQ = L::NQ, NH = L::NH, NT = 128 * NH;
     extern __shared__ __align__(128) float smt[];
     float *fs = smt + L::OFF_FS;
-    float *csb = smt + L::OFF_CS;   // double-buffered: sample b in csb + (b & 1) * 2 T TP
+    float *csb = smt + L::OFF_CS;   // double-buffered: sample b in csb + (b & 1) * 2 T CP
     float *bmat = smt + L::OFF_B;
     float *tr = smt + L::OFF_TR;
     float4 *pfb = reinterpret_cast<float4 *>(smt + L::OFF_PFB);
@@ -1064,7 +1083,7 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
     __syncthreads();   // the previous tile is done with fs, cs, tr and pfb
     for (int e = tid; e < D * T * T; e += NT) {   // centred f tile (reading R12)
         const int c = e / (T * T), i = (e / T) % T, j = e % T;
-        fs[(c * T + i) * TP + j] = a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c];
+        fs[(c * T + i) * CP + j] = a.f[c * plane + (long long)(y0 + i) * W + x0 + j] - a.mu[c];
     }
     if (tid < 4) {
         const int ax = tid >> 1, j = tid & 1;
@@ -1089,16 +1108,16 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
     // (cos, sin) of sample b's phases (Alg. 1) into buffer b & 1: the next sample's
     // modulation runs while this sample's column blur is on the tensor cores
     auto modulate = [&](int b, const float (&tk)[D]) {
-        float *c = csb + (b & 1) * 2 * T * TP;
+        float *c = csb + (b & 1) * 2 * T * CP;
         for (int e = tid; e < T * T; e += NT) {
             const int i = e / T, j = e % T;
             float th = 0.f;
 #pragma unroll
-            for (int cc = 0; cc < D; ++cc) th = fmaf(tk[cc], fs[(cc * T + i) * TP + j], th);
+            for (int cc = 0; cc < D; ++cc) th = fmaf(tk[cc], fs[(cc * T + i) * CP + j], th);
             float sn, cn;
             __sincosf(th, &sn, &cn);
-            c[i * TP + j] = cn;
-            c[T * TP + i * TP + j] = sn;
+            c[i * CP + j] = cn;
+            c[T * CP + i * CP + j] = sn;
         }
     };
     if (s0 < s1) {
@@ -1110,16 +1129,32 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
     }
     __syncthreads();
     for (int b = s0; b < s1; ++b) {
-        const float *cs = csb + (b & 1) * 2 * T * TP;
+        const float *cs = csb + (b & 1) * 2 * T * CP;
         // row operand of line (q, y = lane): the pair's modulated plane (Alg. 1) + row states;
         // part (cos / sin) and pair 0 (no f factor) are warp-uniform: one instance each, no selects
         {
-            const float *hrow = cs + part * T * TP + lane * TP;
-            const float *frow = fs + ((pp > 0 ? pp - 1 : 0) * T + lane) * TP;
+            const float *hrow = cs + part * T * CP + lane * CP;
+            const float *frow = fs + ((pp > 0 ? pp - 1 : 0) * T + lane) * CP;
+#ifdef BFVEC_TC_ROWV4
+            // rows at pitch 36: float4 loads (each quarter-warp phase: 8 distinct 4-bank groups)
+            float xr[T];
+            const float4 *h4 = reinterpret_cast<const float4 *>(hrow), *f4 = reinterpret_cast<const float4 *>(frow);
+#pragma unroll
+            for (int u = 0; u < T / 4; ++u) {
+                float4 h = h4[u];
+                if (pp > 0) {
+                    const float4 fv = f4[u];
+                    h = make_float4(h.x * fv.x, h.y * fv.y, h.z * fv.z, h.w * fv.w);
+                }
+                xr[4 * u] = h.x; xr[4 * u + 1] = h.y; xr[4 * u + 2] = h.z; xr[4 * u + 3] = h.w;
+            }
+            tc_write_operand(tah, tal, [&](int m) -> float { return xr[m]; }, rraw, pfb);
+#else
             if (pp > 0)
                 tc_write_operand(tah, tal, [&](int m) -> float { return hrow[m] * frow[m]; }, rraw, pfb);
             else
                 tc_write_operand(tah, tal, [&](int m) -> float { return hrow[m]; }, rraw, pfb);
+#endif
         }
         if (b + 1 < s1) load_rawp<NQ>(a.Eh, a.Bh, a.UVh, b + 1, qq, tx, y0 + lane, a.ntx, a.nlh, rraw);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1139,14 +1174,19 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
         {
             float y[T];
             tmem_ld32f(td, y);
-            float *trw = tr + (warp * T + lane) * TP;
+            float *trw = tr + (warp * T + lane) * TRP;
+#ifdef BFVEC_TC_TR33
 #pragma unroll
             for (int i = 0; i < T; ++i) trw[i] = y[i];
+#else
+#pragma unroll
+            for (int i = 0; i < T; i += 4) *reinterpret_cast<float4 *>(trw + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+#endif
         }
         __syncwarp();
         {
-            const float *tcol = tr + warp * T * TP + lane;
-            tc_write_operand(tah, tal, [&](int m) -> float { return tcol[m * TP]; }, craw, pfb + 2);
+            const float *tcol = tr + warp * T * TRP + lane;
+            tc_write_operand(tah, tal, [&](int m) -> float { return tcol[m * TRP]; }, craw, pfb + 2);
         }
         if (b + 1 < s1) load_rawp<NQ>(a.Ev, a.Bv, a.UVv, b + 1, qq, ty, x0 + lane, a.nty, W, craw);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1173,9 +1213,9 @@ __global__ void __launch_bounds__(128 * TcSmem<NP>::NH, TcSmem<NP>::NH <= 2 ? 2 
         {
             float z[T];
             tmem_ld32f(td, z);
-            const float *hcol = cs + part * T * TP + lane;
+            const float *hcol = cs + part * T * CP + lane;
 #pragma unroll
-            for (int i = 0; i < T; ++i) acc[i] = fmaf(hcol[i * TP], z[i], acc[i]);
+            for (int i = 0; i < T; ++i) acc[i] = fmaf(hcol[i * CP], z[i], acc[i]);
         }
         __syncthreads();   // sample b + 1's (cos, sin) complete; tr and buffer b & 1 free for reuse
     }
